@@ -1,0 +1,259 @@
+/* pdlp_b200.h — C-ABI boundary of the B200-native restarted-PDHG solver.
+ *
+ * The reference (`pdhglp`, /root/reference/proj/include/pdhglp) is a
+ * header-only C++20 library with no FFI. Its drop-in boundary for the hot
+ * path is the C++ API below; every entry point here replaces one of them:
+ *
+ *   pdlp_create + pdlp_solve      <- pdhglp::solve(const GeneralFormLp&, const SolverParams&)
+ *                                    solver.hpp:935-940 (SolveLoop ctor :636-646, run :759-929)
+ *   pdlp_get_solution             <- SolveResult::point / ::reduced (solver.hpp:618-630)
+ *   pdlp_get_step_log             <- SolveResult::step_log   (StepLogEntry, solver.hpp:596-604)
+ *   pdlp_get_restart_log          <- SolveResult::restart_log (RestartEvent, solver.hpp:606-616)
+ *   pdlp_spmv                     <- spmv / spmv_transpose (sparse_matrix.hpp:117-165)
+ *   pdlp_get_scaling              <- make_scaling(vstack(G,A), ...) (scaling.hpp:117-132)
+ *   pdlp_iterate_begin/run/get    <- SolveLoop::run's loop body, exposed for iterate parity
+ *                                    (solver.hpp:759-841; detail::adaptive_step_cached :381-467)
+ *
+ * Conventions (mirroring the reference):
+ *   - plain pointers and sizes, no C++/torch types; caller-owned inputs are
+ *     read-only and may be freed once pdlp_create returns (they are copied to HBM);
+ *   - every function returns PDLP_OK (0) or an error code and never throws;
+ *     PDLP_EINVAL corresponds to std::invalid_argument in the reference
+ *     (lp_model.hpp:45-72, solver.hpp:79-93), PDLP_ERUNTIME to std::runtime_error;
+ *   - numerical trouble is a *status* (PDLP_STATUS_NUMERICAL_ERROR), not an error code
+ *     (solver.hpp:811-817);
+ *   - one handle per host thread; distinct handles may run concurrently.
+ */
+#ifndef PDLP_B200_H_
+#define PDLP_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PDLP_ABI_VERSION 1
+
+/* ---- return codes ---------------------------------------------------- */
+enum {
+  PDLP_OK = 0,
+  PDLP_EINVAL = 1,   /* std::invalid_argument in the reference */
+  PDLP_ERUNTIME = 2, /* std::runtime_error */
+  PDLP_ECUDA = 3,    /* CUDA / NCCL failure */
+  PDLP_ESTATE = 4    /* call order violated (e.g. get_solution before solve) */
+};
+
+/* ---- SolveStatus (solver.hpp:26-33), same order ----------------------- */
+enum {
+  PDLP_STATUS_OPTIMAL = 0,
+  PDLP_STATUS_PRIMAL_INFEASIBLE = 1,
+  PDLP_STATUS_DUAL_INFEASIBLE = 2,
+  PDLP_STATUS_ITERATION_LIMIT = 3,
+  PDLP_STATUS_TIME_LIMIT = 4,
+  PDLP_STATUS_NUMERICAL_ERROR = 5,
+  PDLP_STATUS_RUNNING = 6 /* only returned by pdlp_iterate_run */
+};
+
+/* ---- RestartCriterion (solver.hpp:47) -------------------------------- */
+enum {
+  PDLP_RESTART_NONE = 0,
+  PDLP_RESTART_SUFFICIENT_DECAY = 1,
+  PDLP_RESTART_NECESSARY_DECAY = 2,
+  PDLP_RESTART_LONG_INNER_LOOP = 3
+};
+
+/* ---- ScalingMode (scaling.hpp:16) ------------------------------------ */
+enum { PDLP_SCALING_NONE = 0, PDLP_SCALING_RUIZ = 1, PDLP_SCALING_RUIZ_PC = 2 };
+
+/* ---- execution modes (B200 extension) -------------------------------- */
+enum {
+  /* Fast deterministic mode: load-balanced tiled SpMV, tree reductions in a
+   * fixed order. Bitwise identical run to run, ~1e-16 relative from the CPU. */
+  PDLP_MODE_FAST = 0,
+  /* Parity mode: every sum is accumulated in the reference's sequential index
+   * order and no FMA is contracted, so iterates are bitwise identical to the
+   * CPU reference. Intended for verification on small instances. */
+  PDLP_MODE_PARITY = 1
+};
+
+/* CSR of one constraint block; mirrors CsrMatrix (sparse_matrix.hpp:35-55).
+ * Invariants expected (as produced by CsrMatrix::from_triplets):
+ * row_offsets[0]==0, row_offsets[num_rows]==nnz, nondecreasing; column indices
+ * strictly increasing within a row; no stored zeros. Indices are 64-bit like
+ * the reference's index_t (sparse_matrix.hpp:21); `col_indices32` may be given
+ * instead of `col_indices` to skip the device-side narrowing. */
+typedef struct {
+  int64_t num_rows;
+  int64_t num_cols;
+  int64_t nnz;
+  const int64_t* row_offsets; /* num_rows + 1 */
+  const int64_t* col_indices; /* nnz, or NULL when col_indices32 is set */
+  const int32_t* col_indices32;
+  const double* values; /* nnz */
+} pdlp_csr;
+
+/* GeneralFormLp (lp_model.hpp:24-43):  min c'x  s.t. Gx >= h, Ax = b, l <= x <= u. */
+typedef struct {
+  pdlp_csr inequality_matrix; /* G, m1 x n */
+  pdlp_csr equality_matrix;   /* A, m2 x n */
+  int64_t num_variables;      /* n */
+  const double* objective;      /* c, n */
+  const double* inequality_rhs; /* h, m1 */
+  const double* equality_rhs;   /* b, m2 */
+  const double* lower;          /* l, n, -inf allowed */
+  const double* upper;          /* u, n, +inf allowed */
+  double objective_constant;
+} pdlp_lp;
+
+/* SolverParams (solver.hpp:59-77), same fields and defaults, plus the B200
+ * execution knobs at the end. Fill with pdlp_default_params first. */
+typedef struct {
+  double eps_optimal;          /* 1e-4 */
+  double eps_infeasible;       /* 1e-8 */
+  double time_limit_seconds;   /* 3600 */
+  int64_t iteration_limit;     /* INT64_MAX */
+  double beta_sufficient;      /* 0.2 */
+  double beta_necessary;       /* 0.8 */
+  double beta_artificial;      /* 0.36 */
+  double theta_smoothing;      /* 0.5 */
+  double eps_zero;             /* 1e-10 */
+  int64_t evaluation_frequency; /* 64 */
+  int32_t scaling;             /* PDLP_SCALING_RUIZ_PC */
+  int32_t ruiz_iterations;     /* 10 */
+  double pock_chambolle_alpha; /* 1.0 */
+  double step_reduction_exponent; /* 0.3 */
+  double step_growth_exponent;    /* 0.6 */
+  double omega_min;            /* 1e-8 */
+  double omega_max;            /* 1e8 */
+  int32_t record_step_log;     /* 0 */
+  /* ---- B200 extensions ---- */
+  int32_t device;              /* CUDA ordinal, default 0 */
+  int32_t mode;                /* PDLP_MODE_FAST */
+  int32_t use_cuda_graph;      /* 1: replay each evaluation window as a CUDA graph */
+  int32_t l2_persist;          /* 1: pin the gathered iterate in L2 (access-policy window) */
+  int32_t reserved[7];
+} pdlp_params;
+
+/* ConvergenceInfo (solver.hpp:165-177) plus SolveResult scalars (:618-630). */
+typedef struct {
+  int32_t status;
+  int32_t has_certificate;
+  int64_t iterations;
+  int64_t restarts;
+  double solve_seconds;  /* loop time, excludes setup like the reference (:636-646,760) */
+  double setup_seconds;  /* upload + K^T build + preconditioning (B200 extension) */
+  double primal_objective;
+  double dual_objective;
+  double primal_objective_raw;
+  double dual_objective_raw;
+  double gap_abs;
+  double primal_residual_norm;
+  double dual_residual_norm;
+  double relative_gap;
+  double relative_primal_residual;
+  double relative_dual_residual;
+  double kkt_omega;
+  int64_t step_log_size;
+  int64_t restart_log_size;
+  int64_t num_variables;
+  int64_t num_constraints;
+  int64_t trials;        /* total line-search trials (B200 extension) */
+  int64_t evaluations;   /* evaluation blocks run (B200 extension) */
+  int64_t gpu_launches;  /* kernels launched by the solve loop (B200 extension) */
+  char message[256];
+} pdlp_result_info;
+
+/* StepLogEntry (solver.hpp:596-604) */
+typedef struct {
+  int64_t step_counter;
+  double omega;
+  double eta_accepted;
+  double eta_bar;
+  double eta_next;
+  double movement_sq;
+  double interaction;
+} pdlp_step_log_entry;
+
+/* RestartEvent (solver.hpp:606-616) */
+typedef struct {
+  int64_t total_iterations;
+  int64_t epoch_length;
+  int32_t criterion;
+  int32_t candidate_is_average;
+  double kkt_candidate;
+  double kkt_previous_candidate;
+  double kkt_epoch_start;
+  double omega_before;
+  double omega_after;
+} pdlp_restart_event;
+
+typedef struct pdlp_handle pdlp_handle;
+
+/* Which operator pdlp_spmv applies. The scaled operator is the saddle
+ * matrix K~ = D1 (G;A) D2 the loop iterates on (solver.hpp:644); the original
+ * one is (G;A) as evaluate_point sees it (lp_model.hpp:184-187,205-207). */
+enum {
+  PDLP_OP_K_SCALED = 0,
+  PDLP_OP_KT_SCALED = 1,
+  PDLP_OP_K_ORIGINAL = 2,
+  PDLP_OP_KT_ORIGINAL = 3
+};
+
+int pdlp_abi_version(void);
+void pdlp_default_params(pdlp_params* params);
+
+/* Validates (GeneralFormLp::validate lp_model.hpp:45-72, SolverParams::validate
+ * solver.hpp:79-93), copies the instance to HBM, builds K^T on the device,
+ * preconditions (Ruiz x ruiz_iterations then Pock-Chambolle) on the device. */
+int pdlp_create(const pdlp_lp* lp, const pdlp_params* params, pdlp_handle** out);
+void pdlp_destroy(pdlp_handle* h);
+
+/* Runs restarted PDHG from z = 0 (solver.hpp:759-929). May be called again:
+ * every call restarts from z = 0 on the resident, preconditioned instance. */
+int pdlp_solve(pdlp_handle* h, pdlp_result_info* info);
+
+/* Result vectors of the last solve (unscaled point or certificate ray, and
+ * its reduced costs). Any pointer may be NULL. x, lambda*: n; y: m. */
+int pdlp_get_solution(pdlp_handle* h, double* x, double* y, double* lambda,
+                      double* lambda_pos, double* lambda_neg);
+int pdlp_get_step_log(pdlp_handle* h, pdlp_step_log_entry* out, int64_t capacity);
+int pdlp_get_restart_log(pdlp_handle* h, pdlp_restart_event* out, int64_t capacity);
+
+/* D1 (m) and D2 (n) of the preconditioner. */
+int pdlp_get_scaling(pdlp_handle* h, double* row_scale, double* col_scale);
+
+/* out = op(in) with host buffers (kernel-level parity). */
+int pdlp_spmv(pdlp_handle* h, int32_t op, const double* in, double* out);
+
+/* Stepwise driving of the same loop pdlp_solve runs (for iterate parity):
+ * begin = initialisation + initial evaluation (solver.hpp:764-792);
+ * run = up to n more accepted iterations, with the evaluation/restart block
+ * whenever the inner counter hits evaluation_frequency; *status receives
+ * PDLP_STATUS_RUNNING or the terminal status. */
+int pdlp_iterate_begin(pdlp_handle* h, int32_t* status);
+int pdlp_iterate_run(pdlp_handle* h, int64_t n, int32_t* status);
+/* Current scaled iterate and its product caches (any pointer may be NULL);
+ * counters = {total k, inner t, outer n, trials}; scalars = {eta, eta_hat, omega,
+ * weight_sum}. */
+int pdlp_get_iterate(pdlp_handle* h, double* x, double* y, double* kx, double* kty,
+                     int64_t* counters, double* scalars);
+
+/* Times `reps` launches of one iteration kernel on the live solver state with
+ * CUDA events on the launching stream (bench roofline). which: 0 = dual
+ * (K x' fused update), 1 = primal (K^T y' fused update). Returns avg ms and the
+ * algorithmic bytes one launch moves. */
+int pdlp_time_kernel(pdlp_handle* h, int32_t which, int32_t reps, double* avg_ms,
+                     double* bytes_per_launch);
+
+/* Problem sizes after create: {n, m, m1, nnz}. */
+int pdlp_get_sizes(pdlp_handle* h, int64_t* sizes);
+
+/* Thread-local message of the last failing call (valid until the next call). */
+const char* pdlp_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PDLP_B200_H_ */

@@ -1,0 +1,166 @@
+// capi.cu — extern "C" boundary (include/pdlp_b200.h). Exceptions never cross
+// it: std::invalid_argument -> PDLP_EINVAL (the reference's error type for bad
+// input, lp_model.hpp:45-72 / solver.hpp:79-93), CUDA failures -> PDLP_ECUDA,
+// everything else -> PDLP_ERUNTIME; the message is kept per thread.
+#include <cstring>
+#include <limits>
+#include <string>
+
+#include "../../include/pdlp_b200.h"
+#include "solver.cuh"
+
+struct pdlp_handle {
+  pdlp::Solver* solver;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return PDLP_OK;
+  } catch (const pdlp::CudaError& e) {
+    g_last_error = e.what();
+    return PDLP_ECUDA;
+  } catch (const std::invalid_argument& e) {
+    g_last_error = e.what();
+    return PDLP_EINVAL;
+  } catch (const std::logic_error& e) {
+    g_last_error = e.what();
+    return PDLP_ESTATE;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return PDLP_ERUNTIME;
+  } catch (...) {
+    g_last_error = "unknown error";
+    return PDLP_ERUNTIME;
+  }
+}
+
+int null_handle() {
+  g_last_error = "null handle";
+  return PDLP_EINVAL;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pdlp_abi_version(void) { return PDLP_ABI_VERSION; }
+
+void pdlp_default_params(pdlp_params* p) {
+  if (!p) return;
+  std::memset(p, 0, sizeof *p);
+  p->eps_optimal = 1e-4;
+  p->eps_infeasible = 1e-8;
+  p->time_limit_seconds = 3600.0;
+  p->iteration_limit = std::numeric_limits<int64_t>::max();
+  p->beta_sufficient = 0.2;
+  p->beta_necessary = 0.8;
+  p->beta_artificial = 0.36;
+  p->theta_smoothing = 0.5;
+  p->eps_zero = 1e-10;
+  p->evaluation_frequency = 64;
+  p->scaling = PDLP_SCALING_RUIZ_PC;
+  p->ruiz_iterations = 10;
+  p->pock_chambolle_alpha = 1.0;
+  p->step_reduction_exponent = 0.3;
+  p->step_growth_exponent = 0.6;
+  p->omega_min = 1e-8;
+  p->omega_max = 1e8;
+  p->record_step_log = 0;
+  p->device = 0;
+  p->mode = PDLP_MODE_FAST;
+  p->use_cuda_graph = 1;
+  p->l2_persist = 1;
+}
+
+int pdlp_create(const pdlp_lp* lp, const pdlp_params* params, pdlp_handle** out) {
+  if (!lp || !params || !out) {
+    g_last_error = "null argument";
+    return PDLP_EINVAL;
+  }
+  *out = nullptr;
+  return guarded([&] {
+    auto* h = new pdlp_handle{nullptr};
+    try {
+      h->solver = new pdlp::Solver(*lp, *params);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+void pdlp_destroy(pdlp_handle* h) {
+  if (!h) return;
+  delete h->solver;
+  delete h;
+}
+
+int pdlp_solve(pdlp_handle* h, pdlp_result_info* info) {
+  if (!h) return null_handle();
+  return guarded([&] { h->solver->solve(info); });
+}
+
+int pdlp_get_solution(pdlp_handle* h, double* x, double* y, double* lambda, double* lambda_pos,
+                      double* lambda_neg) {
+  if (!h) return null_handle();
+  return guarded([&] { h->solver->get_solution(x, y, lambda, lambda_pos, lambda_neg); });
+}
+
+int pdlp_get_step_log(pdlp_handle* h, pdlp_step_log_entry* out, int64_t capacity) {
+  if (!h) return null_handle();
+  return guarded([&] { h->solver->get_step_log(out, capacity); });
+}
+
+int pdlp_get_restart_log(pdlp_handle* h, pdlp_restart_event* out, int64_t capacity) {
+  if (!h) return null_handle();
+  return guarded([&] { h->solver->get_restart_log(out, capacity); });
+}
+
+int pdlp_get_scaling(pdlp_handle* h, double* row_scale, double* col_scale) {
+  if (!h) return null_handle();
+  return guarded([&] { h->solver->get_scaling(row_scale, col_scale); });
+}
+
+int pdlp_spmv(pdlp_handle* h, int32_t op, const double* in, double* out) {
+  if (!h) return null_handle();
+  return guarded([&] { h->solver->spmv(op, in, out); });
+}
+
+int pdlp_iterate_begin(pdlp_handle* h, int32_t* status) {
+  if (!h) return null_handle();
+  return guarded([&] { h->solver->iterate_begin(status); });
+}
+
+int pdlp_iterate_run(pdlp_handle* h, int64_t n, int32_t* status) {
+  if (!h) return null_handle();
+  return guarded([&] { h->solver->iterate_run(n, status); });
+}
+
+int pdlp_get_iterate(pdlp_handle* h, double* x, double* y, double* kx, double* kty,
+                     int64_t* counters, double* scalars) {
+  if (!h) return null_handle();
+  return guarded([&] { h->solver->get_iterate(x, y, kx, kty, counters, scalars); });
+}
+
+int pdlp_time_kernel(pdlp_handle* h, int32_t which, int32_t reps, double* avg_ms,
+                     double* bytes_per_launch) {
+  if (!h) return null_handle();
+  return guarded([&] { h->solver->time_kernel(which, reps, avg_ms, bytes_per_launch); });
+}
+
+int pdlp_get_sizes(pdlp_handle* h, int64_t* sizes) {
+  if (!h) return null_handle();
+  return guarded([&] { h->solver->sizes(sizes); });
+}
+
+const char* pdlp_last_error(void) { return g_last_error.c_str(); }
+
+}  // extern "C"

@@ -1,0 +1,121 @@
+// common.cuh — error handling and deterministic reduction helpers shared by
+// the sm_100a kernels of the restarted-PDHG hot path.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace pdlp {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct InvalidArgument : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+
+#define PDLP_CUDA(expr)                                                                  \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess)                                                               \
+      throw ::pdlp::CudaError(std::string(#expr) + ": " + cudaGetErrorString(_e) + " @" + \
+                              __FILE__ + ":" + std::to_string(__LINE__));                \
+  } while (0)
+
+constexpr int kThreads = 256;        // CTA size of every tiled kernel
+constexpr int kWarps = kThreads / 32;
+constexpr int kStreamNnz = 2048;     // nnz staged per STREAM tile (8 per thread)
+constexpr int kStreamMaxRow = 32;    // rows up to this length go to STREAM tiles
+constexpr int kWarpMaxRow = 512;     // (32, 512] -> one warp per row, 8 rows per tile
+constexpr int kChunkNnz = 4096;      // longer rows split into chunks of this many nnz
+constexpr int kVecPad = 8;           // index/value arrays padded for 128-bit tail loads
+
+// ---------------------------------------------------------------------------
+// IEEE helpers with the reference's semantics (libstdc++ std::min/std::max are
+// ternaries that propagate a NaN first argument; CUDA fmin/fmax drop NaN).
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }
+__host__ __device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }
+
+// Streaming loads of matrix data: not reused within a launch, keep out of L1.
+__device__ __forceinline__ int4 ld_stream_i4(const int* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ double2 ld_stream_d2(const double* p) {
+  double2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
+               : "=d"(r.x), "=d"(r.y)
+               : "l"(p));
+  return r;
+}
+
+// Fixed-order warp sum (xor butterfly): identical result on every replay.
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Fixed-order block sum of K doubles per thread; result valid in thread 0.
+// Warp butterflies, then warp partials summed by thread 0 in warp order.
+template <int K>
+__device__ __forceinline__ void block_sum(double (&v)[K], double* smem /* kWarps*K */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < K; ++i) v[i] = warp_sum(v[i]);
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) smem[warp * K + i] = v[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      double s = smem[i];
+      for (int w = 1; w < kWarps; ++w) s += smem[w * K + i];
+      v[i] = s;
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Fixed-order block reduction: the first NS entries are summed, the last NM are
+// max-reduced (maxima never see NaN: callers only store guarded comparisons).
+template <int NS, int NM>
+__device__ __forceinline__ void block_reduce(double (&v)[NS + NM], double* smem /* kWarps*(NS+NM) */) {
+  constexpr int K = NS + NM;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < K; ++i) v[i] = i < NS ? warp_sum(v[i]) : warp_max(v[i]);
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) smem[warp * K + i] = v[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      double s = smem[i];
+      for (int w = 1; w < kWarps; ++w) s = i < NS ? s + smem[w * K + i] : fmax(s, smem[w * K + i]);
+      v[i] = s;
+    }
+  }
+  __syncthreads();
+}
+
+}  // namespace pdlp

@@ -1,0 +1,122 @@
+// device_state.h — layouts shared by the host runtime and the kernels.
+#pragma once
+
+#include <stdint.h>
+
+#include "tiles.h"
+
+namespace pdlp {
+
+// Which branch the primal kernel takes (set by the dual kernel's decision).
+enum PMode : int32_t { kPNone = 0, kPAccept = 1, kPRetry = 2, kPRestart = 3 };
+
+// Scalar solver state resident in HBM. The host owns the fields above the
+// marker between windows (uploads them before a window), the kernels own the
+// rest during a window (downloaded after it).
+struct DevState {
+  double eta;       // step size of the next trial (eta-hat at a step start)
+  double omega;     // primal weight
+  double wsum;      // WeightedAverage weight sum (vector_ops.hpp:95-107)
+  int64_t total;    // k
+  int64_t inner;    // t
+  int64_t table_base;  // total at window start (index base of the factor table)
+  int32_t window_target;
+  int32_t p_mode;
+  int32_t ix_cur, ix_prev, ix_trial;  // rotation of the three x buffers
+  int32_t iy_cur, iy_prev, iy_trial;  // rotation of the three y buffers
+  int32_t ikx_cur, ikty_cur;          // rotation of the two Kx / K'y buffers
+  int32_t record_log;
+  int32_t pad0;
+  // ---- kernel-owned during a window ----
+  int32_t window_accepts;
+  int32_t trials_in_step;
+  int64_t trials_total;
+  int32_t failure;
+  int32_t accepted;
+  double avg_ratio;
+  int32_t avg_first;
+  int32_t pad1;
+  double eta_acc, eta_bar, eta_next, mov, inter;  // last accepted step
+  unsigned ctr_dual;
+  unsigned ctr_eval;
+};
+
+// Results of one evaluation block (evaluate_candidates + the infeasibility
+// rays, solver.hpp:705-739, :853-885) for four points carried side by side:
+// slot 0 = current, 1 = average, 2 = last-step delta ray, 3 = normalized ray.
+struct EvalOut {
+  // KKT points (slots 0, 1): KktResiduals (solver.hpp:109-123)
+  double prn[2], drn[2], pobj[2], dobj[2];
+  // rays (slots 2, 3): certificate_from_ray (solver.hpp:503-574)
+  double y_norm[2], kty_resid[2], ray_dobj[2];
+  double x_norm[2], ax_norm[2], gx_negmax[2], xl_negmax[2], xu_max[2], cx[2];
+  // restart displacement of each candidate vs the epoch start (scaled space)
+  double dx2[2], dy2[2];
+};
+
+// Device pointers of one CSR operator with its tile plan.
+struct DevCsr {
+  const int* rp;
+  const int* col;
+  const double* val;       // scaled (iteration) values
+  const double* val_orig;  // original values (evaluation)
+  int rows;
+  int cols;
+  int64_t nnz;
+  const Tile* tiles;
+  int ntiles;
+  int chunk_slots;
+  double* chunk_part;     // [chunk_slots * 8]
+  unsigned* chunk_ctr;    // [split_rows]
+};
+
+// Vectors of the iteration (all device pointers, fixed for the graph's life).
+struct DevIter {
+  double* x[3];
+  double* y[3];
+  double* kx[2];
+  double* kty[2];
+  double* avg_x;
+  double* avg_y;
+  double* x_start;
+  double* y_start;
+  const double* c;   // scaled objective
+  const double* l;   // scaled bounds
+  const double* u;
+  const double* q;   // scaled rhs (h; b)
+  int n, m, m1;
+  int p_grid;        // CTAs of the primal kernel
+  int avg_blocks;    // trailing CTAs of the primal kernel that update avg_y
+  double* d_part;    // [K tiles * 3]
+  double* p_part;    // [p_grid * 2]
+  double* seq_dy2;   // parity-mode per-row terms (m)
+  double* seq_inter; // (m)
+  double* seq_dx2;   // (n)
+  const double* red_tab;  // reduction factors 1-(k+1)^-0.3 for the window
+  const double* gro_tab;  // growth factors 1+(k+1)^-0.6
+  void* step_log;         // pdlp_step_log_entry[window capacity]
+  DevState* st;
+};
+
+// Vectors of the evaluation block.
+struct DevEval {
+  double* X4;   // [n][4] unscaled x of the four points
+  double* Y4;   // [m][4] unscaled y (rays projected onto the dual cone)
+  double* lam;  // [4][n] reduced costs lambda of the four points
+  const double* c;   // original objective
+  const double* l;   // original bounds
+  const double* u;
+  const double* q;   // original rhs (h; b)
+  const double* d1;  // row scale
+  const double* d2;  // col scale
+  double objective_constant;
+  double* part0;  // EV0 partials [grid0 * 4]
+  double* part1;  // EV1 partials [K tiles * 14]
+  double* part2;  // EV2 partials [KT tiles * 18]
+  int grid0;
+  double* seq_r;  // parity: [4][m] row residual terms
+  double* seq_d;  // parity: [4][n] column residual terms
+  EvalOut* out;
+};
+
+}  // namespace pdlp

@@ -1,0 +1,1080 @@
+// kernels.cu — sm_100a kernels of the restarted-PDHG hot path.
+//
+// Reference routine each kernel replaces (paths relative to
+// /root/reference/proj/include/pdhglp/):
+//   dual_kernel     adaptive_step_cached trial: spmv(K, x') solver.hpp:409, the
+//                   dual update :410-415, all_finite :417-420, dy^2/interaction
+//                   :428-435, eta_bar / eta' / accept :436-466 (last CTA), plus the
+//                   WeightedAverage weight bookkeeping (vector_ops.hpp:95-107).
+//   primal_kernel   accept: spmv_transpose(K, y') :456 as a gather over the stored
+//                   K^T, fused with avg_x/avg_y .add (solver.hpp:838-839) and the
+//                   NEXT trial's primal update :404-408 and dx^2 :422-427;
+//                   reject: the primal update alone for the shrunk step.
+//   eval_*          evaluate_candidates (solver.hpp:705-739) for current + average
+//                   and check_infeasibility's two rays (:581-590) in one pass over
+//                   K and one over K^T, four points side by side.
+//   setup kernels   from_triplets/explicit_transpose/vstack (sparse_matrix.hpp:57-200),
+//                   ruiz/pock-chambolle/apply_scaling (scaling.hpp:32-170).
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "../../include/pdlp_b200.h"
+#include "kernels.cuh"
+#include "spmv_engine.cuh"
+
+namespace pdlp {
+
+namespace {
+
+__device__ __forceinline__ double clamp_box(double v, double l, double u) {
+  return smin(smax(v, l), u);  // std::min(std::max(x, l), u), vector_ops.hpp:56
+}
+
+// reduced_costs_from_slack (lp_model.hpp:155-174), one component.
+__device__ __forceinline__ double reduced_cost(double v, double l, double u) {
+  const bool lf = l > -INFINITY, uf = u < INFINITY;
+  if (lf && uf) return v;
+  if (lf) return smax(v, 0.0);
+  if (uf) return smin(v, 0.0);
+  return 0.0;
+}
+
+// l'lambda+ - u'lambda- contribution of one component (lp_model.hpp:248-251).
+__device__ __forceinline__ double lambda_term(double lam, double l, double u) {
+  if (lam > 0.0) return l * lam;
+  if (lam < 0.0) return -(u * -lam);
+  return 0.0;
+}
+
+int ceil_div(int64_t a, int64_t b) { return int((a + b - 1) / b); }
+
+}  // namespace
+
+// ===========================================================================
+// Iteration: dual kernel
+// ===========================================================================
+
+template <bool kSeq>
+struct DualEpi {
+  static constexpr int NP = 1, NA = 1, NR = 3;
+  static constexpr bool kNeedCol = false;
+  const double* __restrict__ xg;
+  const double* __restrict__ y;
+  const double* __restrict__ kx;
+  const double* __restrict__ q;
+  double* __restrict__ yt;
+  double* __restrict__ kxt;
+  double* __restrict__ seq_dy2;
+  double* __restrict__ seq_inter;
+  double sigma;
+  int m1;
+  __device__ __forceinline__ void gather(int c, double (&g)[1]) const { g[0] = __ldg(xg + c); }
+  __device__ __forceinline__ void add(double (&a)[1], const double (&p)[1], int) const { a[0] += p[0]; }
+  __device__ __forceinline__ void row_done(int r, const double (&a)[1], double (&red)[3]) const {
+    const double kxn = a[0];
+    const double kxo = kx[r], yo = y[r];
+    double yn = yo + sigma * (q[r] - 2.0 * kxn + kxo);  // solver.hpp:412-413
+    if (r < m1 && yn < 0.0) yn = 0.0;                    // project_dual_in_place
+    yt[r] = yn;
+    kxt[r] = kxn;
+    const double d = yn - yo;
+    const double dd = d * d, di = d * (kxn - kxo);
+    if (kSeq) {
+      seq_dy2[r] = dd;
+      seq_inter[r] = di;
+    }
+    red[0] += dd;
+    red[1] += di;
+    red[2] += isfinite(yn) ? 0.0 : 1.0;
+  }
+};
+
+// Sequential (reference-order) sums used by the parity mode's reductions.
+__device__ double seq_sum(const double* v, int n) {
+  double s = 0.0;
+  for (int i = 0; i < n; ++i) s += __ldcg(v + i);
+  return s;
+}
+__device__ double seq_sum_sq(const double* v, int n) {
+  double s = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double a = __ldcg(v + i);
+    s += a * a;
+  }
+  return s;
+}
+
+template <bool kSeq>
+__global__ void __launch_bounds__(kThreads) dual_kernel(DevCsr K, DevIter it,
+                                                        cudaGraphConditionalHandle cond,
+                                                        int use_cond) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  DevState* st = it.st;
+  // A failed or completed window parks the remaining (fallback-mode) launches.
+  if (st->failure || st->window_accepts >= st->window_target) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->p_mode = kPNone;
+    return;
+  }
+  DualEpi<kSeq> epi;
+  epi.xg = it.x[st->ix_trial];
+  epi.y = it.y[st->iy_cur];
+  epi.kx = it.kx[st->ikx_cur];
+  epi.q = it.q;
+  epi.yt = it.y[st->iy_trial];
+  epi.kxt = it.kx[1 - st->ikx_cur];
+  epi.seq_dy2 = it.seq_dy2;
+  epi.seq_inter = it.seq_inter;
+  epi.sigma = st->eta * st->omega;  // sigma = eta * omega, solver.hpp:402
+  epi.m1 = it.m1;
+  double red[3] = {0.0, 0.0, 0.0};
+  const Tile t = K.tiles[blockIdx.x];
+  run_tile<DualEpi<kSeq>, kSeq>(t, K.rp, K.col, K.val, epi, red, K.chunk_part, K.chunk_ctr, smem);
+  store_partial<3, 0>(red, it.d_part, blockIdx.x);
+  if (!grid_last_block(&st->ctr_dual, gridDim.x)) return;
+
+  // ---- last CTA: reductions and the step decision ----
+  double dpart[3], ppart[2];
+  sum_partials<3, 0>(it.d_part, gridDim.x, dpart);
+  sum_partials<2, 0>(it.p_part, it.p_grid, ppart);
+  if (threadIdx.x != 0) return;
+  double dy2 = dpart[0], inter = dpart[1], dx2 = ppart[0];
+  if (kSeq) {  // the reference's sequential index order (solver.hpp:422-435)
+    dx2 = seq_sum(it.seq_dx2, it.n);
+    double a = 0.0, b = 0.0;
+    for (int i = 0; i < it.m; ++i) {
+      a += __ldcg(it.seq_dy2 + i);
+      b += __ldcg(it.seq_inter + i);
+    }
+    dy2 = a;
+    inter = b;
+  }
+  const bool finite = dpart[2] == 0.0 && ppart[1] == 0.0;
+  const double omega = st->omega, eta = st->eta;
+  int cont = 0;
+  st->trials_total += 1;
+  st->trials_in_step += 1;
+  if (!finite) {
+    st->failure = 1;
+    st->p_mode = kPNone;
+  } else {
+    const double movement = omega * dx2 + dy2 / omega;  // solver.hpp:436
+    const double ia = fabs(inter);
+    const double eta_bar = ia > 0.0 ? movement / (2.0 * ia) : INFINITY;
+    const int64_t ti = st->total - st->table_base;
+    const double eta_next = smin(it.red_tab[ti] * eta_bar, it.gro_tab[ti] * eta);
+    if (eta <= eta_bar) {
+      if (st->record_log) {
+        pdlp_step_log_entry* log = reinterpret_cast<pdlp_step_log_entry*>(it.step_log);
+        pdlp_step_log_entry e;
+        e.step_counter = st->total + 1;
+        e.omega = omega;
+        e.eta_accepted = eta;
+        e.eta_bar = eta_bar;
+        e.eta_next = eta_next;
+        e.movement_sq = movement;
+        e.interaction = inter;
+        log[st->window_accepts] = e;
+      }
+      st->eta_acc = eta;
+      st->eta_bar = eta_bar;
+      st->eta_next = eta_next;
+      st->mov = movement;
+      st->inter = inter;
+      st->total += 1;
+      st->inner += 1;
+      st->window_accepts += 1;
+      const double w = st->wsum + eta;  // WeightedAverage::add
+      st->wsum = w;
+      st->avg_first = (w == eta) ? 1 : 0;
+      st->avg_ratio = eta / w;
+      // rotate: prev <- cur <- trial <- old prev
+      int t0 = st->ix_prev;
+      st->ix_prev = st->ix_cur;
+      st->ix_cur = st->ix_trial;
+      st->ix_trial = t0;
+      t0 = st->iy_prev;
+      st->iy_prev = st->iy_cur;
+      st->iy_cur = st->iy_trial;
+      st->iy_trial = t0;
+      st->ikx_cur = 1 - st->ikx_cur;
+      st->ikty_cur = 1 - st->ikty_cur;
+      st->eta = eta_next;
+      st->trials_in_step = 0;
+      st->accepted = 1;
+      st->p_mode = kPAccept;
+      cont = st->window_accepts < st->window_target;
+    } else {
+      st->eta = eta_next;
+      st->accepted = 0;
+      if (!(eta_next > 0.0) || !isfinite(eta_next) || st->trials_in_step >= 80) {
+        st->failure = 1;
+        st->p_mode = kPNone;
+      } else {
+        st->p_mode = kPRetry;
+        cont = 1;
+      }
+    }
+  }
+  __threadfence();
+  if (use_cond) cudaGraphSetConditional(cond, cont ? 1u : 0u);
+}
+
+// ===========================================================================
+// Iteration: primal kernel
+// ===========================================================================
+
+template <bool kSeq>
+struct PrimalEpi {
+  static constexpr int NP = 1, NA = 1, NR = 2;
+  static constexpr bool kNeedCol = false;
+  const double* __restrict__ yg;
+  const double* __restrict__ xc;
+  const double* __restrict__ c;
+  const double* __restrict__ l;
+  const double* __restrict__ u;
+  double* __restrict__ kty_out;
+  double* __restrict__ xt;
+  double* __restrict__ avg_x;
+  double* __restrict__ seq_dx2;
+  double tau;
+  double ratio;
+  int do_avg;
+  int avg_first;
+  __device__ __forceinline__ void gather(int r, double (&g)[1]) const { g[0] = __ldg(yg + r); }
+  __device__ __forceinline__ void add(double (&a)[1], const double (&p)[1], int) const { a[0] += p[0]; }
+  __device__ __forceinline__ void row_done(int j, const double (&a)[1], double (&red)[2]) const {
+    const double s = a[0];
+    kty_out[j] = s;
+    const double xa = xc[j];
+    if (do_avg) avg_x[j] = avg_first ? xa : avg_x[j] + ratio * (xa - avg_x[j]);
+    const double xn = clamp_box(xa - tau * (c[j] - s), l[j], u[j]);  // solver.hpp:404-408
+    xt[j] = xn;
+    const double d = xn - xa;
+    const double dd = d * d;
+    if (kSeq) seq_dx2[j] = dd;
+    red[0] += dd;
+    red[1] += isfinite(xn) ? 0.0 : 1.0;
+  }
+};
+
+template <bool kSeq>
+__global__ void __launch_bounds__(kThreads) primal_kernel(DevCsr KT, DevIter it, int mode_override) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const DevState* st = it.st;
+  const int mode = mode_override >= 0 ? mode_override : st->p_mode;
+  if (mode == kPNone) return;  // keep the partials of the last real trial
+  double red[2] = {0.0, 0.0};
+  const double tau = st->eta / st->omega;  // tau = eta / omega, solver.hpp:401
+  const int bid = blockIdx.x;
+  if (mode == kPAccept || mode == kPRestart) {
+    const bool acc = mode == kPAccept;
+    if (bid < KT.ntiles) {
+      PrimalEpi<kSeq> epi;
+      epi.yg = it.y[st->iy_cur];
+      epi.xc = it.x[st->ix_cur];
+      epi.c = it.c;
+      epi.l = it.l;
+      epi.u = it.u;
+      epi.kty_out = it.kty[st->ikty_cur];
+      epi.xt = it.x[st->ix_trial];
+      epi.avg_x = it.avg_x;
+      epi.seq_dx2 = it.seq_dx2;
+      epi.tau = tau;
+      epi.ratio = st->avg_ratio;
+      epi.do_avg = acc;
+      epi.avg_first = st->avg_first;
+      const Tile t = KT.tiles[bid];
+      run_tile<PrimalEpi<kSeq>, kSeq>(t, KT.rp, KT.col, KT.val, epi, red, KT.chunk_part,
+                                      KT.chunk_ctr, smem);
+    } else if (acc) {
+      // avg_y .add (solver.hpp:839) on this CTA's slice of the dual vector
+      const int nb = it.avg_blocks, b = bid - KT.ntiles;
+      const int per = (it.m + nb - 1) / nb;
+      const int i0 = b * per, i1 = min(it.m, i0 + per);
+      const double* yc = it.y[st->iy_cur];
+      const double ratio = st->avg_ratio;
+      const int first = st->avg_first;
+      for (int i = i0 + threadIdx.x; i < i1; i += kThreads)
+        it.avg_y[i] = first ? yc[i] : it.avg_y[i] + ratio * (yc[i] - it.avg_y[i]);
+    }
+  } else if (mode == kPRetry) {
+    const int per = (it.n + gridDim.x - 1) / gridDim.x;
+    const int j0 = bid * per, j1 = min(it.n, j0 + per);
+    const double* xc = it.x[st->ix_cur];
+    const double* kty = it.kty[st->ikty_cur];
+    double* xt = it.x[st->ix_trial];
+    for (int j = j0 + threadIdx.x; j < j1; j += kThreads) {
+      const double xa = xc[j];
+      const double xn = clamp_box(xa - tau * (it.c[j] - kty[j]), it.l[j], it.u[j]);
+      xt[j] = xn;
+      const double d = xn - xa;
+      const double dd = d * d;
+      if (kSeq) it.seq_dx2[j] = dd;
+      red[0] += dd;
+      red[1] += isfinite(xn) ? 0.0 : 1.0;
+    }
+  }
+  store_partial<2, 0>(red, it.p_part, bid);
+}
+
+// ===========================================================================
+// Plain SpMV (kernel parity API and restart products)
+// ===========================================================================
+
+struct MatvecEpi {
+  static constexpr int NP = 1, NA = 1, NR = 1;
+  static constexpr bool kNeedCol = false;
+  const double* __restrict__ x;
+  double* __restrict__ out;
+  __device__ __forceinline__ void gather(int c, double (&g)[1]) const { g[0] = __ldg(x + c); }
+  __device__ __forceinline__ void add(double (&a)[1], const double (&p)[1], int) const { a[0] += p[0]; }
+  __device__ __forceinline__ void row_done(int r, const double (&a)[1], double (&)[1]) const {
+    out[r] = a[0];
+  }
+};
+
+template <bool kSeq>
+__global__ void __launch_bounds__(kThreads) spmv_kernel(DevCsr A, const double* val,
+                                                        const double* x, double* out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  MatvecEpi epi{x, out};
+  double red[1] = {0.0};
+  const Tile t = A.tiles[blockIdx.x];
+  run_tile<MatvecEpi, kSeq>(t, A.rp, A.col, val, epi, red, A.chunk_part, A.chunk_ctr, smem);
+}
+
+__global__ void zero_iterate_kernel(DevIter it) {
+  const DevState* st = it.st;
+  double* x = it.x[st->ix_cur];
+  double* y = it.y[st->iy_cur];
+  double* kx = it.kx[st->ikx_cur];
+  double* kty = it.kty[st->ikty_cur];
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < it.n; j += stride) {
+    x[j] = 0.0;
+    kty[j] = 0.0;
+    it.x_start[j] = 0.0;
+    it.avg_x[j] = 0.0;
+    it.x[st->ix_prev][j] = 0.0;
+  }
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < it.m; i += stride) {
+    y[i] = 0.0;
+    kx[i] = 0.0;
+    it.y_start[i] = 0.0;
+    it.avg_y[i] = 0.0;
+    it.y[st->iy_prev][i] = 0.0;
+  }
+}
+
+// Restart block (solver.hpp:907-909): z_start = z = candidate (current or average).
+__global__ void restart_copy_kernel(DevIter it, int from_avg) {
+  const DevState* st = it.st;
+  double* x = it.x[st->ix_cur];
+  double* y = it.y[st->iy_cur];
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < it.n; j += stride) {
+    const double v = from_avg ? it.avg_x[j] : x[j];
+    x[j] = v;
+    it.x_start[j] = v;
+  }
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < it.m; i += stride) {
+    const double v = from_avg ? it.avg_y[i] : y[i];
+    y[i] = v;
+    it.y_start[i] = v;
+  }
+}
+
+// ===========================================================================
+// Evaluation block
+// ===========================================================================
+
+// EV0: unscaled copies of the four points (unscale_point, scaling.hpp:174-184),
+// and the restart displacement ||cand - z_start||^2 of both candidates.
+constexpr int kEv0Items = 4;  // elements per thread per block pass
+
+__global__ void __launch_bounds__(kThreads) eval_prep_kernel(DevIter it, DevEval ev, int xblocks) {
+  const DevState* st = it.st;
+  const bool empty = st->wsum == 0.0;
+  const double inv_t = st->inner > 0 ? 1.0 / double(st->inner) : 0.0;
+  double red[4] = {0.0, 0.0, 0.0, 0.0};
+  const int span = kThreads * kEv0Items;
+  if (int(blockIdx.x) < xblocks) {
+    const double* xc = it.x[st->ix_cur];
+    const double* xp = it.x[st->ix_prev];
+    const double* xa = empty ? xc : it.avg_x;
+    const int j0 = blockIdx.x * span, j1 = min(it.n, j0 + span);
+    for (int j = j0 + threadIdx.x; j < j1; j += kThreads) {
+      const double d2 = ev.d2[j], c = xc[j], a = xa[j], s = it.x_start[j];
+      double2* dst = reinterpret_cast<double2*>(ev.X4 + size_t(j) * 4);
+      dst[0] = make_double2(c * d2, a * d2);
+      dst[1] = make_double2((c - xp[j]) * d2, (inv_t * (c - s)) * d2);
+      const double dc = c - s, da = a - s;
+      red[0] += dc * dc;
+      red[1] += da * da;
+    }
+  } else {
+    const double* yc = it.y[st->iy_cur];
+    const double* yp = it.y[st->iy_prev];
+    const double* ya = empty ? yc : it.avg_y;
+    const int b = blockIdx.x - xblocks;
+    const int i0 = b * span, i1 = min(it.m, i0 + span);
+    for (int i = i0 + threadIdx.x; i < i1; i += kThreads) {
+      const double d1 = ev.d1[i], c = yc[i], a = ya[i], s = it.y_start[i];
+      double r2 = (c - yp[i]) * d1;
+      double r3 = (inv_t * (c - s)) * d1;
+      if (i < it.m1) {  // certificate_from_ray projects the ray (solver.hpp:509-510)
+        if (r2 < 0.0) r2 = 0.0;
+        if (r3 < 0.0) r3 = 0.0;
+      }
+      double2* dst = reinterpret_cast<double2*>(ev.Y4 + size_t(i) * 4);
+      dst[0] = make_double2(c * d1, a * d1);
+      dst[1] = make_double2(r2, r3);
+      const double dc = c - s, da = a - s;
+      red[2] += dc * dc;
+      red[3] += da * da;
+    }
+  }
+  store_partial<4, 0>(red, ev.part0, blockIdx.x);
+}
+
+int eval_grid0(int n, int m) {
+  const int span = kThreads * kEv0Items;
+  return ceil_div(n, span) + ceil_div(m, span);
+}
+
+__device__ __forceinline__ void load4(const double* p, double (&g)[4]) {
+  const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+  const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+  g[0] = a.x;
+  g[1] = a.y;
+  g[2] = b.x;
+  g[3] = b.y;
+}
+
+// EV1 over rows of the ORIGINAL (G; A): primal residuals (lp_model.hpp:202-218),
+// q'y (lp_model.hpp:240-247), ray tests on Ax/Gx and ||y|| (solver.hpp:509-566).
+// Reductions: [0..5] KKT slots (viol^2, eq^2, q'y) x2, [6..11] ray slots
+// (|Ax|^2, |y|^2, q'y) x2; maxima [12..13]: max_i(-Gx_i) per ray.
+template <bool kSeq>
+struct Ev1Epi {
+  static constexpr int NP = 4, NA = 4, NR = 14;
+  static constexpr bool kNeedCol = false;
+  const double* __restrict__ X4;
+  const double* __restrict__ Y4;
+  const double* __restrict__ q;
+  double* __restrict__ seq_r;
+  int m, m1;
+  __device__ __forceinline__ void gather(int c, double (&g)[4]) const { load4(X4 + size_t(c) * 4, g); }
+  __device__ __forceinline__ void add(double (&a)[4], const double (&p)[4], int) const {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] += p[i];
+  }
+  __device__ __forceinline__ void row_done(int r, const double (&a)[4], double (&red)[14]) const {
+    const double qr = q[r];
+    if (r < m1) {
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const double v = smax(qr - a[s], 0.0);  // [h - Gx]+
+        red[s * 3 + 0] += v * v;
+        if (kSeq) seq_r[size_t(s) * m + r] = v;
+      }
+#pragma unroll
+      for (int s = 2; s < 4; ++s) {
+        const double ng = -a[s];
+        if (ng > red[12 + s - 2]) red[12 + s - 2] = ng;
+      }
+    } else {
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const double v = a[s] + -1.0 * qr;  // Ax + (-1) b, axpy order
+        red[s * 3 + 1] += v * v;
+        if (kSeq) seq_r[size_t(s) * m + r] = v;
+      }
+#pragma unroll
+      for (int s = 2; s < 4; ++s) {
+        red[6 + (s - 2) * 3 + 0] += a[s] * a[s];
+        if (kSeq) seq_r[size_t(s) * m + r] = a[s];
+      }
+    }
+    double y[4];
+    load4(Y4 + size_t(r) * 4, y);
+    red[2] += qr * y[0];
+    red[5] += qr * y[1];
+    red[7] += y[2] * y[2];
+    red[8] += qr * y[2];
+    red[10] += y[3] * y[3];
+    red[11] += qr * y[3];
+  }
+};
+
+// EV2 over rows of the ORIGINAL K^T, G- and A-parts summed separately as
+// dual_slack does (lp_model.hpp:179-190). Reductions: KKT slots (|c-K'y-lam|^2,
+// c'x, lambda terms) x2 = [0..5]; ray slots (|K'y+lam|^2, lambda terms, |x|^2,
+// c'x) x2 = [6..13]; maxima [14..17]: (max -x over finite l, max x over finite u)
+// per ray.
+template <bool kSeq>
+struct Ev2Epi {
+  static constexpr int NP = 4, NA = 8, NR = 18;
+  static constexpr bool kNeedCol = true;
+  const double* __restrict__ Y4;
+  const double* __restrict__ X4;
+  const double* __restrict__ c;
+  const double* __restrict__ l;
+  const double* __restrict__ u;
+  double* __restrict__ lam;
+  double* __restrict__ seq_d;
+  int n, m1;
+  __device__ __forceinline__ void gather(int r, double (&g)[4]) const { load4(Y4 + size_t(r) * 4, g); }
+  __device__ __forceinline__ void add(double (&a)[8], const double (&p)[4], int col) const {
+    if (col < m1) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] += p[i];
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[4 + i] += p[i];
+    }
+  }
+  __device__ __forceinline__ void row_done(int j, const double (&a)[8], double (&red)[18]) const {
+    const double cj = c[j], lj = l[j], uj = u[j];
+    double x[4];
+    load4(X4 + size_t(j) * 4, x);
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const double slack = (cj + -1.0 * a[s]) + -1.0 * a[4 + s];
+      const double lm = reduced_cost(slack, lj, uj);
+      lam[size_t(s) * n + j] = lm;
+      const double dres = slack + -1.0 * lm;
+      if (kSeq) seq_d[size_t(s) * n + j] = dres;
+      red[s * 3 + 0] += dres * dres;
+      red[s * 3 + 1] += cj * x[s];
+      red[s * 3 + 2] += lambda_term(lm, lj, uj);
+    }
+#pragma unroll
+    for (int s = 2; s < 4; ++s) {
+      const double kty = a[s] + 1.0 * a[4 + s];
+      const double lm = reduced_cost(-kty, lj, uj);
+      lam[size_t(s) * n + j] = lm;
+      const double viol = kty + 1.0 * lm;
+      if (kSeq) seq_d[size_t(s) * n + j] = viol;
+      const int o = 6 + (s - 2) * 4;
+      red[o + 0] += viol * viol;
+      red[o + 1] += lambda_term(lm, lj, uj);
+      red[o + 2] += x[s] * x[s];
+      red[o + 3] += cj * x[s];
+      const int mo = 14 + (s - 2) * 2;
+      if (lj > -INFINITY && -x[s] > red[mo]) red[mo] = -x[s];
+      if (uj < INFINITY && x[s] > red[mo + 1]) red[mo + 1] = x[s];
+    }
+  }
+};
+
+template <bool kSeq>
+__global__ void __launch_bounds__(kThreads) eval_rows_kernel(DevCsr K, DevEval ev, int m, int m1) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  Ev1Epi<kSeq> epi{ev.X4, ev.Y4, ev.q, ev.seq_r, m, m1};
+  double red[14];
+#pragma unroll
+  for (int i = 0; i < 14; ++i) red[i] = i < 12 ? 0.0 : -INFINITY;
+  const Tile t = K.tiles[blockIdx.x];
+  run_tile<Ev1Epi<kSeq>, kSeq>(t, K.rp, K.col, K.val_orig, epi, red, K.chunk_part, K.chunk_ctr, smem);
+  store_partial<12, 2>(red, ev.part1, blockIdx.x);
+}
+
+template <bool kSeq>
+__global__ void __launch_bounds__(kThreads) eval_cols_kernel(DevCsr KT, DevEval ev, int n, int m1) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  Ev2Epi<kSeq> epi{ev.Y4, ev.X4, ev.c, ev.l, ev.u, ev.lam, ev.seq_d, n, m1};
+  double red[18];
+#pragma unroll
+  for (int i = 0; i < 18; ++i) red[i] = i < 14 ? 0.0 : -INFINITY;
+  const Tile t = KT.tiles[blockIdx.x];
+  run_tile<Ev2Epi<kSeq>, kSeq>(t, KT.rp, KT.col, KT.val_orig, epi, red, KT.chunk_part, KT.chunk_ctr,
+                              smem);
+  store_partial<14, 4>(red, ev.part2, blockIdx.x);
+}
+
+// Parity-mode dual objective: the single sequential accumulator of
+// dual_objective (lp_model.hpp:236-253) minus the constant.
+__device__ double seq_dual_objective(const DevEval& ev, int slot, int n, int m) {
+  double obj = ev.objective_constant;
+  for (int i = 0; i < m; ++i) obj += ev.q[i] * ev.Y4[size_t(i) * 4 + slot];
+  const double* lam = ev.lam + size_t(slot) * n;
+  for (int j = 0; j < n; ++j) {
+    const double v = lam[j];
+    if (v > 0.0) obj += ev.l[j] * v;
+    if (v < 0.0) obj -= ev.u[j] * -v;
+  }
+  return obj - ev.objective_constant;
+}
+
+template <bool kSeq>
+__global__ void __launch_bounds__(kThreads) eval_final_kernel(DevEval ev, int grid1, int grid2,
+                                                              int n, int m, int m1) {
+  double p0[4], p1[14], p2[18];
+  sum_partials<4, 0>(ev.part0, ev.grid0, p0);
+  sum_partials<12, 2>(ev.part1, grid1, p1);
+  sum_partials<14, 4>(ev.part2, grid2, p2);
+  EvalOut* o = ev.out;
+  const double c0 = ev.objective_constant;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) {
+      o->prn[s] = sqrt(p1[s * 3 + 1] + p1[s * 3 + 0]);  // sqrt(|eq|^2 + |viol|^2)
+      o->drn[s] = sqrt(p2[s * 3 + 0]);
+      o->pobj[s] = p2[s * 3 + 1];
+      o->dobj[s] = ((c0 + p1[s * 3 + 2]) + p2[s * 3 + 2]) - c0;
+    }
+    for (int r = 0; r < 2; ++r) {
+      o->ax_norm[r] = sqrt(p1[6 + r * 3 + 0]);
+      o->y_norm[r] = sqrt(p1[6 + r * 3 + 1]);
+      o->kty_resid[r] = sqrt(p2[6 + r * 4 + 0]);
+      o->ray_dobj[r] = ((c0 + p1[6 + r * 3 + 2]) + p2[6 + r * 4 + 1]) - c0;
+      o->x_norm[r] = sqrt(p2[6 + r * 4 + 2]);
+      o->cx[r] = p2[6 + r * 4 + 3];
+      o->gx_negmax[r] = p1[12 + r];
+      o->xl_negmax[r] = p2[14 + r * 2];
+      o->xu_max[r] = p2[14 + r * 2 + 1];
+    }
+    o->dx2[0] = p0[0];
+    o->dx2[1] = p0[1];
+    o->dy2[0] = p0[2];
+    o->dy2[1] = p0[3];
+  }
+  if (!kSeq) return;
+  __syncthreads();
+  // Parity mode: every sum in the reference's sequential order, one thread per sum.
+  const int t = threadIdx.x;
+  if (t < 2) {  // primal residual of the KKT points
+    const double* r = ev.seq_r + size_t(t) * m;
+    double eq = 0.0, vi = 0.0;
+    for (int i = m1; i < m; ++i) eq += r[i] * r[i];
+    for (int i = 0; i < m1; ++i) vi += r[i] * r[i];
+    o->prn[t] = sqrt(eq + vi);
+  } else if (t < 4) {
+    const int s = t - 2;
+    o->drn[s] = sqrt(seq_sum_sq(ev.seq_d + size_t(s) * n, n));
+  } else if (t < 6) {
+    const int s = t - 4;
+    double a = 0.0;
+    for (int j = 0; j < n; ++j) a += ev.c[j] * ev.X4[size_t(j) * 4 + s];
+    o->pobj[s] = a;
+  } else if (t < 8) {
+    o->dobj[t - 6] = seq_dual_objective(ev, t - 6, n, m);
+  } else if (t < 10) {
+    const int s = t - 8 + 2;
+    double a = 0.0;
+    for (int i = 0; i < m; ++i) a += ev.Y4[size_t(i) * 4 + s] * ev.Y4[size_t(i) * 4 + s];
+    o->y_norm[s - 2] = sqrt(a);
+  } else if (t < 12) {
+    const int s = t - 10 + 2;
+    o->kty_resid[s - 2] = sqrt(seq_sum_sq(ev.seq_d + size_t(s) * n, n));
+  } else if (t < 14) {
+    const int s = t - 12 + 2;
+    o->ray_dobj[s - 2] = seq_dual_objective(ev, s, n, m);
+  } else if (t < 16) {
+    const int s = t - 14 + 2;
+    double a = 0.0;
+    for (int j = 0; j < n; ++j) a += ev.X4[size_t(j) * 4 + s] * ev.X4[size_t(j) * 4 + s];
+    o->x_norm[s - 2] = sqrt(a);
+  } else if (t < 18) {
+    const int s = t - 16 + 2;
+    const double* r = ev.seq_r + size_t(s) * m;
+    double a = 0.0;
+    for (int i = m1; i < m; ++i) a += r[i] * r[i];
+    o->ax_norm[s - 2] = sqrt(a);
+  } else if (t < 20) {
+    const int s = t - 18 + 2;
+    double a = 0.0;
+    for (int j = 0; j < n; ++j) a += ev.c[j] * ev.X4[size_t(j) * 4 + s];
+    o->cx[s - 2] = a;
+  }
+}
+
+// Parity-mode restart displacement (update_primal_weight, solver.hpp:309-317).
+__global__ void eval_seq_displacement_kernel(DevIter it, EvalOut* o) {
+  const DevState* st = it.st;
+  const bool empty = st->wsum == 0.0;
+  const int t = threadIdx.x;
+  if (t < 2) {
+    const double* xc = it.x[st->ix_cur];
+    const double* v = (t == 1 && !empty) ? it.avg_x : xc;
+    double a = 0.0;
+    for (int j = 0; j < it.n; ++j) {
+      const double d = v[j] - it.x_start[j];
+      a += d * d;
+    }
+    o->dx2[t] = a;
+  } else if (t < 4) {
+    const double* yc = it.y[st->iy_cur];
+    const double* v = (t == 3 && !empty) ? it.avg_y : yc;
+    double a = 0.0;
+    for (int i = 0; i < it.m; ++i) {
+      const double d = v[i] - it.y_start[i];
+      a += d * d;
+    }
+    o->dy2[t - 2] = a;
+  }
+}
+
+// reduced_costs(lp, 0) for a dual-infeasibility exit (solver.hpp:877): slack = c.
+__global__ void reduced_of_objective_kernel(const double* c, const double* l, const double* u,
+                                            int n, double* lam) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+    lam[j] = reduced_cost((c[j] + -1.0 * 0.0) + -1.0 * 0.0, l[j], u[j]);
+}
+
+// ===========================================================================
+// Setup kernels
+// ===========================================================================
+
+__global__ void build_rowptr_kernel(const int64_t* g_off, const int64_t* a_off, int64_t m1,
+                                    int64_t m2, int64_t nnz_g, int* rp) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i <= m1 + m2; i += stride) {
+    rp[i] = i <= m1 ? int(g_off[i]) : int(a_off[i - m1] + nnz_g);
+  }
+}
+
+__global__ void narrow_cols_kernel(const int64_t* c64, int* c32, int64_t nnz, int n, int* err) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < nnz; k += stride) {
+    const int64_t v = c64[k];
+    if (v < 0 || v >= n) atomicOr(err, 1);
+    c32[k] = int(v);
+  }
+}
+
+__global__ void check_cols_kernel(const int* c32, int64_t nnz, int n, int* err) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < nnz; k += stride) {
+    const int v = c32[k];
+    if (v < 0 || v >= n) atomicOr(err, 1);
+  }
+}
+
+// CSR invariants (sparse_matrix.hpp:29-34): nondecreasing offsets, strictly
+// increasing columns within a row.
+__global__ void check_rows_kernel(const int* rp, const int* col, int rows, int* err) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+    const int a = rp[r], b = rp[r + 1];
+    if (b < a) {
+      atomicOr(err, 2);
+      continue;
+    }
+    for (int k = a + 1; k < b; ++k)
+      if (col[k] <= col[k - 1]) {
+        atomicOr(err, 4);
+        break;
+      }
+  }
+}
+
+__global__ void expand_rows_kernel(const int* rp, int rows, int* row_of) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x)
+    for (int k = rp[r]; k < rp[r + 1]; ++k) row_of[k] = r;
+}
+
+__global__ void iota_kernel(int* p, int64_t n) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += stride) p[k] = int(k);
+}
+
+__global__ void count_cols_kernel(const int* col, int64_t nnz, int* counts) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < nnz; k += stride)
+    atomicAdd(counts + col[k], 1);
+}
+
+__global__ void gather_transpose_kernel(const int* perm, const int* row_of, const double* val,
+                                        int64_t nnz, int* col_t, double* val_t) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < nnz; k += stride) {
+    const int p = perm[k];
+    col_t[k] = row_of[p];
+    val_t[k] = val[p];
+  }
+}
+
+__global__ void fill_kernel(double* p, int64_t n, double v) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += stride) p[k] = v;
+}
+
+__global__ void fill_int_kernel(int* p, int64_t n, int v) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += stride) p[k] = v;
+}
+
+// One warp per row: max |v * (d_self[r] * d_other[col])| (order-free, exact).
+__global__ void row_absmax_kernel(const int* rp, const int* col, const double* val, int rows,
+                                  const double* d_self, const double* d_other, double* out) {
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int r = warp; r < rows; r += nwarps) {
+    const double dr = d_self[r];
+    double mx = 0.0;
+    for (int k = rp[r] + lane; k < rp[r + 1]; k += 32) {
+      // scaled_copy multiplies v *= dr * dc (scaling.hpp:38-40)
+      const double a = fabs(val[k] * (dr * d_other[col[k]]));
+      mx = smax(mx, a);
+    }
+    mx = warp_max(mx);
+    if (lane == 0) out[r] = mx;
+  }
+}
+
+// Thread per row, sequential in index order (row_norms / col_norms accumulate
+// in that order, sparse_matrix.hpp:214-248), then the p-norm root.
+__global__ void row_pnorm_kernel(const int* rp, const int* col, const double* val, int rows,
+                                 const double* d_self, const double* d_other, double p,
+                                 double* out) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+    const double dr = d_self[r];
+    double acc = 0.0;
+    for (int k = rp[r]; k < rp[r + 1]; ++k) {
+      const double a = fabs(val[k] * (dr * d_other[col[k]]));
+      if (p == 0.0)
+        acc += 1.0;
+      else if (p == 1.0)
+        acc += a;  // pow(a, 1.0) == a exactly
+      else
+        acc += pow(a, p);
+    }
+    if (p != 0.0 && p != 1.0 && acc > 0.0) acc = pow(acc, 1.0 / p);
+    out[r] = acc;
+  }
+}
+
+__global__ void ruiz_update_kernel(double* d, const double* norm, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double v = norm[i];
+    if (v > 0.0) d[i] /= sqrt(v);
+  }
+}
+
+// pock_chambolle_scale + compose (scaling.hpp:83-111): d *= 1/sqrt(sum^p).
+__global__ void pc_update_kernel(double* d, const double* sum, int n, double p) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double s = sum[i];
+    if (p != 0.0 && p != 1.0 && s > 0.0) s = pow(s, p);
+    const double pc = s > 0.0 ? 1.0 / sqrt(s) : 1.0;
+    d[i] *= pc;
+  }
+}
+
+__global__ void scale_values_kernel(const int* rp, const int* col, const double* val, int rows,
+                                    const double* d_self, const double* d_other, double* out) {
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int r = warp; r < rows; r += nwarps) {
+    const double dr = d_self[r];
+    for (int k = rp[r] + lane; k < rp[r + 1]; k += 32) out[k] = val[k] * (dr * d_other[col[k]]);
+  }
+}
+
+// apply_scaling on the vectors (scaling.hpp:158-168).
+__global__ void scale_vectors_kernel(const double* c, const double* l, const double* u,
+                                     const double* q, const double* d1, const double* d2, int n,
+                                     int m, double* cs, double* ls, double* us, double* qs) {
+  const int stride = gridDim.x * blockDim.x;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
+    const double s = d2[j];
+    cs[j] = c[j] * s;
+    ls[j] = isfinite(l[j]) ? l[j] / s : l[j];
+    us[j] = isfinite(u[j]) ? u[j] / s : u[j];
+  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) qs[i] = q[i] * d1[i];
+}
+
+__global__ void block_absmax_kernel(const double* v, int64_t n, double* partials) {
+  __shared__ double sred[kWarps];
+  double mx = 0.0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += stride)
+    mx = smax(mx, fabs(v[k]));
+  double a[1] = {mx};
+  block_reduce<0, 1>(a, sred);
+  if (threadIdx.x == 0) partials[blockIdx.x] = a[0];
+}
+
+// ===========================================================================
+// Launchers
+// ===========================================================================
+
+namespace {
+int grid_for(int64_t n, int per = kThreads) {
+  int64_t g = (n + per - 1) / per;
+  if (g < 1) g = 1;
+  if (g > 148 * 16) g = 148 * 16;
+  return int(g);
+}
+}  // namespace
+
+void set_kernel_attributes() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  auto big = [](const void* f, size_t bytes) {
+    PDLP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+  };
+  big((const void*)eval_rows_kernel<false>, stream_smem_bytes<Ev1Epi<false>>());
+  big((const void*)eval_rows_kernel<true>, stream_smem_bytes<Ev1Epi<true>>());
+  big((const void*)eval_cols_kernel<false>, stream_smem_bytes<Ev2Epi<false>>());
+  big((const void*)eval_cols_kernel<true>, stream_smem_bytes<Ev2Epi<true>>());
+}
+
+void launch_build_rowptr(const int64_t* g_off, const int64_t* a_off, int64_t m1, int64_t m2,
+                         int64_t nnz_g, int* rp, cudaStream_t s) {
+  build_rowptr_kernel<<<grid_for(m1 + m2 + 1), kThreads, 0, s>>>(g_off, a_off, m1, m2, nnz_g, rp);
+  PDLP_CUDA(cudaGetLastError());
+}
+void launch_narrow_cols(const int64_t* col64, int* col32, int64_t nnz, int n, int* err,
+                        cudaStream_t s) {
+  narrow_cols_kernel<<<grid_for(nnz), kThreads, 0, s>>>(col64, col32, nnz, n, err);
+  PDLP_CUDA(cudaGetLastError());
+}
+void launch_check_cols(const int* col32, int64_t nnz, int n, int* err, cudaStream_t s) {
+  check_cols_kernel<<<grid_for(nnz), kThreads, 0, s>>>(col32, nnz, n, err);
+  PDLP_CUDA(cudaGetLastError());
+}
+void launch_check_rows(const int* rp, const int* col, int rows, int* err, cudaStream_t s) {
+  check_rows_kernel<<<grid_for(rows), kThreads, 0, s>>>(rp, col, rows, err);
+  PDLP_CUDA(cudaGetLastError());
+}
+void launch_expand_rows(const int* rp, int rows, int* row_of, cudaStream_t s) {
+  expand_rows_kernel<<<grid_for(rows), kThreads, 0, s>>>(rp, rows, row_of);
+  PDLP_CUDA(cudaGetLastError());
+}
+void launch_iota(int* p, int64_t n, cudaStream_t s) {
+  iota_kernel<<<grid_for(n), kThreads, 0, s>>>(p, n);
+  PDLP_CUDA(cudaGetLastError());
+}
+void launch_count_cols(const int* col, int64_t nnz, int* counts, cudaStream_t s) {
+  count_cols_kernel<<<grid_for(nnz), kThreads, 0, s>>>(col, nnz, counts);
+  PDLP_CUDA(cudaGetLastError());
+}
+void launch_gather_transpose(const int* perm, const int* row_of, const double* val, int64_t nnz,
+                             int* col_t, double* val_t, cudaStream_t s) {
+  gather_transpose_kernel<<<grid_for(nnz), kThreads, 0, s>>>(perm, row_of, val, nnz, col_t, val_t);
+  PDLP_CUDA(cudaGetLastError());
+}
+void launch_fill(double* p, int64_t n, double v, cudaStream_t s) {
+  fill_kernel<<<grid_for(n), kThreads, 0, s>>>(p, n, v);
+  PDLP_CUDA(cudaGetLastError());
+}
+void launch_fill_int(int* p, int64_t n, int v, cudaStream_t s) {
+  fill_int_kernel<<<grid_for(n), kThreads, 0, s>>>(p, n, v);
+  PDLP_CUDA(cudaGetLastError());
+}
+void launch_row_absmax(const int* rp, const int* col, const double* val, int rows,
+                       const double* d_self, const double* d_other, double* out, cudaStream_t s) {
+  row_absmax_kernel<<<grid_for(int64_t(rows) * 32), kThreads, 0, s>>>(rp, col, val, rows, d_self,
+                                                                     d_other, out);
+  PDLP_CUDA(cudaGetLastError());
+}
+void launch_row_pnorm(const int* rp, const int* col, const double* val, int rows,
+                      const double* d_self, const double* d_other, double p, double* out,
+                      cudaStream_t s) {
+  row_pnorm_kernel<<<grid_for(rows, 128), 128, 0, s>>>(rp, col, val, rows, d_self, d_other, p, out);
+  PDLP_CUDA(cudaGetLastError());
+}
+void launch_ruiz_update(double* d, const double* norm, int n, cudaStream_t s) {
+  ruiz_update_kernel<<<grid_for(n), kThreads, 0, s>>>(d, norm, n);
+  PDLP_CUDA(cudaGetLastError());
+}
+void launch_pc_update(double* d, const double* sum, int n, double p, cudaStream_t s) {
+  pc_update_kernel<<<grid_for(n), kThreads, 0, s>>>(d, sum, n, p);
+  PDLP_CUDA(cudaGetLastError());
+}
+void launch_scale_values(const int* rp, const int* col, const double* val_orig, int rows,
+                         const double* d_self, const double* d_other, double* val_out,
+                         cudaStream_t s) {
+  scale_values_kernel<<<grid_for(int64_t(rows) * 32), kThreads, 0, s>>>(rp, col, val_orig, rows,
+                                                                       d_self, d_other, val_out);
+  PDLP_CUDA(cudaGetLastError());
+}
+void launch_scale_vectors(const double* c, const double* l, const double* u, const double* q,
+                          const double* d1, const double* d2, int n, int m, double* cs,
+                          double* ls, double* us, double* qs, cudaStream_t s) {
+  scale_vectors_kernel<<<grid_for(n > m ? n : m), kThreads, 0, s>>>(c, l, u, q, d1, d2, n, m, cs, ls,
+                                                                   us, qs);
+  PDLP_CUDA(cudaGetLastError());
+}
+void launch_block_absmax(const double* v, int64_t n, double* partials, int nblocks,
+                         cudaStream_t s) {
+  block_absmax_kernel<<<nblocks, kThreads, 0, s>>>(v, n, partials);
+  PDLP_CUDA(cudaGetLastError());
+}
+
+void launch_spmv(const DevCsr& a, bool orig_vals, const double* x, double* out, bool seq,
+                 cudaStream_t s) {
+  if (a.ntiles == 0) return;
+  const size_t sm = stream_smem_bytes<MatvecEpi>();
+  const double* val = orig_vals ? a.val_orig : a.val;
+  if (seq)
+    spmv_kernel<true><<<a.ntiles, kThreads, sm, s>>>(a, val, x, out);
+  else
+    spmv_kernel<false><<<a.ntiles, kThreads, sm, s>>>(a, val, x, out);
+  PDLP_CUDA(cudaGetLastError());
+}
+
+void launch_dual(const DevCsr& k, const DevIter& it, bool seq, unsigned long long cond,
+                 int use_cond, cudaStream_t s) {
+  const size_t sm = stream_smem_bytes<DualEpi<false>>();
+  cudaGraphConditionalHandle h = static_cast<cudaGraphConditionalHandle>(cond);
+  if (seq)
+    dual_kernel<true><<<k.ntiles, kThreads, sm, s>>>(k, it, h, use_cond);
+  else
+    dual_kernel<false><<<k.ntiles, kThreads, sm, s>>>(k, it, h, use_cond);
+  PDLP_CUDA(cudaGetLastError());
+}
+
+void launch_primal(const DevCsr& kt, const DevIter& it, bool seq, int mode_override,
+                   cudaStream_t s) {
+  const size_t sm = stream_smem_bytes<PrimalEpi<false>>();
+  if (seq)
+    primal_kernel<true><<<it.p_grid, kThreads, sm, s>>>(kt, it, mode_override);
+  else
+    primal_kernel<false><<<it.p_grid, kThreads, sm, s>>>(kt, it, mode_override);
+  PDLP_CUDA(cudaGetLastError());
+}
+
+void launch_zero_iterate(const DevIter& it, cudaStream_t s) {
+  zero_iterate_kernel<<<grid_for(it.n > it.m ? it.n : it.m), kThreads, 0, s>>>(it);
+  PDLP_CUDA(cudaGetLastError());
+}
+
+void launch_restart_copy(const DevIter& it, int from_avg, cudaStream_t s) {
+  restart_copy_kernel<<<grid_for(it.n > it.m ? it.n : it.m), kThreads, 0, s>>>(it, from_avg);
+  PDLP_CUDA(cudaGetLastError());
+}
+
+void launch_eval(const DevCsr& k, const DevCsr& kt, const DevIter& it, const DevEval& ev, bool seq,
+                 cudaStream_t s) {
+  const int span = kThreads * kEv0Items;
+  const int xblocks = ceil_div(it.n, span);
+  eval_prep_kernel<<<ev.grid0, kThreads, 0, s>>>(it, ev, xblocks);
+  PDLP_CUDA(cudaGetLastError());
+  const size_t sm1 = stream_smem_bytes<Ev1Epi<false>>();
+  const size_t sm2 = stream_smem_bytes<Ev2Epi<false>>();
+  if (seq) {
+    if (k.ntiles) eval_rows_kernel<true><<<k.ntiles, kThreads, sm1, s>>>(k, ev, it.m, it.m1);
+    if (kt.ntiles) eval_cols_kernel<true><<<kt.ntiles, kThreads, sm2, s>>>(kt, ev, it.n, it.m1);
+    eval_final_kernel<true><<<1, kThreads, 0, s>>>(ev, k.ntiles, kt.ntiles, it.n, it.m, it.m1);
+    eval_seq_displacement_kernel<<<1, 32, 0, s>>>(it, ev.out);
+  } else {
+    if (k.ntiles) eval_rows_kernel<false><<<k.ntiles, kThreads, sm1, s>>>(k, ev, it.m, it.m1);
+    if (kt.ntiles) eval_cols_kernel<false><<<kt.ntiles, kThreads, sm2, s>>>(kt, ev, it.n, it.m1);
+    eval_final_kernel<false><<<1, kThreads, 0, s>>>(ev, k.ntiles, kt.ntiles, it.n, it.m, it.m1);
+  }
+  PDLP_CUDA(cudaGetLastError());
+}
+
+void launch_reduced_of_objective(const double* c, const double* l, const double* u, int n,
+                                 double* lam, cudaStream_t s) {
+  reduced_of_objective_kernel<<<grid_for(n), kThreads, 0, s>>>(c, l, u, n, lam);
+  PDLP_CUDA(cudaGetLastError());
+}
+
+}  // namespace pdlp

@@ -1,0 +1,66 @@
+// kernels.cuh — declarations of the host-side launchers in kernels.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "device_state.h"
+
+namespace pdlp {
+
+// ---- setup -----------------------------------------------------------------
+void launch_build_rowptr(const int64_t* g_off, const int64_t* a_off, int64_t m1, int64_t m2,
+                         int64_t nnz_g, int* rp, cudaStream_t s);
+void launch_narrow_cols(const int64_t* col64, int* col32, int64_t nnz, int n, int* err,
+                        cudaStream_t s);
+void launch_check_cols(const int* col32, int64_t nnz, int n, int* err, cudaStream_t s);
+void launch_check_rows(const int* rp, const int* col, int rows, int* err, cudaStream_t s);
+void launch_expand_rows(const int* rp, int rows, int* row_of, cudaStream_t s);
+void launch_iota(int* p, int64_t n, cudaStream_t s);
+void launch_count_cols(const int* col, int64_t nnz, int* counts, cudaStream_t s);
+void launch_gather_transpose(const int* perm, const int* row_of, const double* val, int64_t nnz,
+                             int* col_t, double* val_t, cudaStream_t s);
+void launch_fill(double* p, int64_t n, double v, cudaStream_t s);
+void launch_fill_int(int* p, int64_t n, int v, cudaStream_t s);
+// Ruiz (scaling.hpp:52-66): out[r] = max_k |v_k * (d_row[r] * d_col[col_k])|
+void launch_row_absmax(const int* rp, const int* col, const double* val, int rows,
+                       const double* d_self, const double* d_other, double* out, cudaStream_t s);
+// Pock-Chambolle (scaling.hpp:72-94): out[r] = sequential sum_k |v*(d*d)|^p, then the
+// row's pow(acc, 1/p) exactly as row_norms/col_norms (sparse_matrix.hpp:212-255)
+void launch_row_pnorm(const int* rp, const int* col, const double* val, int rows,
+                      const double* d_self, const double* d_other, double p, double* out,
+                      cudaStream_t s);
+void launch_ruiz_update(double* d, const double* norm, int n, cudaStream_t s);
+void launch_pc_update(double* d, const double* sum, int n, double p, cudaStream_t s);
+void launch_scale_values(const int* rp, const int* col, const double* val_orig, int rows,
+                         const double* d_self, const double* d_other, double* val_out,
+                         cudaStream_t s);
+void launch_scale_vectors(const double* c, const double* l, const double* u, const double* q,
+                          const double* d1, const double* d2, int n, int m, double* cs,
+                          double* ls, double* us, double* qs, cudaStream_t s);
+void launch_block_absmax(const double* v, int64_t n, double* partials, int nblocks,
+                         cudaStream_t s);
+
+// ---- iteration -------------------------------------------------------------
+// out = A x with the tiled engine (parity: sequential rows, fast: tiled).
+void launch_spmv(const DevCsr& a, bool orig_vals, const double* x, double* out, bool seq,
+                 cudaStream_t s);
+// Trial of adaptive_step_cached (solver.hpp:404-466) on the dual side, plus the
+// step decision; sets the WHILE condition when `cond` != 0.
+void launch_dual(const DevCsr& k, const DevIter& it, bool seq, unsigned long long cond,
+                 int use_cond, cudaStream_t s);
+// Primal side: K'y' + average + next trial x' (mode from state, or forced).
+void launch_primal(const DevCsr& kt, const DevIter& it, bool seq, int mode_override,
+                   cudaStream_t s);
+void launch_zero_iterate(const DevIter& it, cudaStream_t s);
+void launch_restart_copy(const DevIter& it, int from_avg, cudaStream_t s);
+
+// ---- evaluation ------------------------------------------------------------
+void launch_eval(const DevCsr& k, const DevCsr& kt, const DevIter& it, const DevEval& ev,
+                 bool seq, cudaStream_t s);
+int eval_grid0(int n, int m);
+void launch_reduced_of_objective(const double* c, const double* l, const double* u, int n,
+                                 double* lam, cudaStream_t s);
+
+void set_kernel_attributes();
+
+}  // namespace pdlp

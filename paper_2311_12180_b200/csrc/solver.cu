@@ -1,0 +1,920 @@
+// solver.cu — host runtime: upload, K^T build, preconditioning, the windowed
+// iteration loop replayed as a CUDA graph, and the evaluation/restart logic.
+//
+// Mirrors pdhglp::detail::SolveLoop (solver.hpp:634-929). Division of labour:
+//   device: every O(nnz) and O(n + m) pass (SpMVs, projections, averages,
+//           residuals, reductions) and the per-trial step decision;
+//   host:   once per evaluation window (64 accepted iterations by default), the
+//           O(1) scalar logic on ~30 reduced numbers: KKT_omega, candidate
+//           choice, termination, Farkas tests, restart criteria and the primal
+//           weight (glibc exp/log, bitwise with the reference), plus the
+//           per-window table of glibc pow step factors (solver.hpp:388-390).
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+
+#include "kernels.cuh"
+#include "solver.cuh"
+
+namespace pdlp {
+
+namespace {
+
+double sclamp(double v, double lo, double hi) { return (v < lo) ? lo : ((hi < v) ? hi : v); }
+
+[[noreturn]] void invalid(const std::string& m) { throw InvalidArgument(m); }
+
+void validate_params(const pdlp_params& p) {  // SolverParams::validate, solver.hpp:79-93
+  if (!(p.eps_optimal > 0.0) || !(p.eps_infeasible > 0.0))
+    invalid("params: tolerances must be positive");
+  if (!(p.beta_sufficient > 0.0 && p.beta_sufficient < p.beta_necessary && p.beta_necessary < 1.0))
+    invalid("params: need 0 < beta_sufficient < beta_necessary < 1");
+  if (p.theta_smoothing < 0.0 || p.theta_smoothing > 1.0)
+    invalid("params: theta_smoothing must lie in [0, 1]");
+  if (p.evaluation_frequency < 1) invalid("params: evaluation_frequency must be >= 1");
+  if (p.ruiz_iterations < 0) invalid("ruiz: negative iteration count");
+  if (p.pock_chambolle_alpha < 0.0 || p.pock_chambolle_alpha > 2.0)
+    invalid("pock-chambolle: alpha must lie in [0, 2]");
+  if (p.mode != PDLP_MODE_FAST && p.mode != PDLP_MODE_PARITY) invalid("params: unknown mode");
+}
+
+double seq_norm2(const std::vector<double>& v) {
+  double s = 0.0;
+  for (double x : v) s += x * x;
+  return std::sqrt(s);
+}
+
+}  // namespace
+
+double KktHost::weighted(double omega) const {  // KktResiduals::weighted
+  const double pr = omega * prn, dr = drn / omega, g = gap();
+  return std::sqrt(pr * pr + dr * dr + g * g);
+}
+
+// ---------------------------------------------------------------------------
+// construction
+// ---------------------------------------------------------------------------
+
+Solver::Solver(const pdlp_lp& lp, const pdlp_params& params) : params_(params) {
+  const auto t = std::chrono::steady_clock::now();
+  PDLP_CUDA(cudaSetDevice(params.device));
+  PDLP_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  setup(lp);
+  PDLP_CUDA(cudaStreamSynchronize(stream_));
+  setup_seconds_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - t).count();
+}
+
+Solver::~Solver() {
+  if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+  if (graph_) cudaGraphDestroy(graph_);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Solver::setup(const pdlp_lp& lp) {
+  // ---- GeneralFormLp::validate (lp_model.hpp:45-72), then params ----
+  const pdlp_csr& G = lp.inequality_matrix;
+  const pdlp_csr& A = lp.equality_matrix;
+  n_ = lp.num_variables;
+  if (n_ < 0 || G.num_rows < 0 || A.num_rows < 0 || G.nnz < 0 || A.nnz < 0)
+    invalid("lp: negative dimension");
+  if (G.num_cols != n_ || A.num_cols != n_) invalid("lp: constraint matrices must have n columns");
+  m1_ = G.num_rows;
+  m2_ = A.num_rows;
+  m_ = m1_ + m2_;
+  nnz_ = G.nnz + A.nnz;
+  auto need = [](const void* p, int64_t len, const char* what) {
+    if (len > 0 && !p) invalid(std::string("lp: missing ") + what);
+  };
+  need(lp.objective, n_, "objective");
+  need(lp.lower, n_, "lower bounds");
+  need(lp.upper, n_, "upper bounds");
+  need(lp.inequality_rhs, m1_, "inequality rhs");
+  need(lp.equality_rhs, m2_, "equality rhs");
+  for (const pdlp_csr* c : {&G, &A}) {
+    need(c->values, c->nnz, "matrix values");
+    if (c->nnz > 0 && !c->col_indices && !c->col_indices32) invalid("lp: missing column indices");
+    if (c->num_rows > 0 && !c->row_offsets) invalid("lp: missing row offsets");
+    if (c->row_offsets && (c->row_offsets[0] != 0 || c->row_offsets[c->num_rows] != c->nnz))
+      invalid("csr: row_offsets must start at 0 and end at nnz");
+  }
+  for (int64_t i = 0; i < n_; ++i) {
+    const double l = lp.lower[i], u = lp.upper[i];
+    if (std::isnan(l) || std::isnan(u)) invalid("lp: NaN bound on variable " + std::to_string(i));
+    if (l > u || l == INFINITY || u == -INFINITY)
+      invalid("lp: empty bound interval on variable " + std::to_string(i));
+  }
+  for (int64_t i = 0; i < n_; ++i)
+    if (std::isnan(lp.objective[i])) invalid("lp: NaN objective entry");
+  validate_params(params_);
+  const int64_t lim = int64_t(std::numeric_limits<int32_t>::max()) - 1024;
+  if (n_ > lim || m_ > lim || nnz_ > lim)
+    throw std::runtime_error("instance exceeds the 32-bit index layout of one device (shard it)");
+
+  objective_constant_ = lp.objective_constant;
+  c_.assign(lp.objective, lp.objective + n_);
+  l_.assign(lp.lower, lp.lower + n_);
+  u_.assign(lp.upper, lp.upper + n_);
+  q_.resize(m_);
+  std::copy(lp.inequality_rhs, lp.inequality_rhs + m1_, q_.begin());
+  std::copy(lp.equality_rhs, lp.equality_rhs + m2_, q_.begin() + m1_);
+  {  // termination_norms on the ORIGINAL instance (solver.hpp:157-163)
+    double sh = 0.0, sb = 0.0, sc = 0.0;
+    for (int64_t i = 0; i < m1_; ++i) sh += q_[i] * q_[i];
+    for (int64_t i = m1_; i < m_; ++i) sb += q_[i] * q_[i];
+    for (double v : c_) sc += v * v;
+    rhs_norm_ = std::sqrt(sh + sb);
+    obj_norm_ = std::sqrt(sc);
+  }
+
+  cudaStream_t s = stream_;
+  // ---- K = vstack(G, A) (sparse_matrix.hpp:181-200) in HBM, int32 indices ----
+  k_rp_.alloc(m_ + 1);
+  k_col_.alloc(nnz_ + kVecPad);
+  k_val_orig_.alloc(nnz_ + kVecPad);
+  k_val_.alloc(nnz_ + kVecPad);
+  k_col_.zero(s);
+  k_val_orig_.zero(s);
+  k_val_.zero(s);
+  DevBuf<int64_t> goff(m1_ + 1), aoff(m2_ + 1);
+  std::vector<int64_t> zero_off{0};
+  PDLP_CUDA(cudaMemcpyAsync(goff.get(), G.row_offsets ? G.row_offsets : zero_off.data(),
+                            (m1_ + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  PDLP_CUDA(cudaMemcpyAsync(aoff.get(), A.row_offsets ? A.row_offsets : zero_off.data(),
+                            (m2_ + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  launch_build_rowptr(goff.get(), aoff.get(), m1_, m2_, G.nnz, k_rp_.get(), s);
+  DevBuf<int> err(1);
+  err.zero(s);
+  int64_t off = 0;
+  for (const pdlp_csr* c : {&G, &A}) {
+    if (c->nnz > 0) {
+      if (c->col_indices32) {
+        PDLP_CUDA(cudaMemcpyAsync(k_col_.get() + off, c->col_indices32, c->nnz * sizeof(int),
+                                  cudaMemcpyHostToDevice, s));
+      } else {
+        DevBuf<int64_t> tmp(c->nnz);
+        PDLP_CUDA(cudaMemcpyAsync(tmp.get(), c->col_indices, c->nnz * sizeof(int64_t),
+                                  cudaMemcpyHostToDevice, s));
+        launch_narrow_cols(tmp.get(), k_col_.get() + off, c->nnz, int(n_), err.get(), s);
+        PDLP_CUDA(cudaStreamSynchronize(s));
+      }
+      PDLP_CUDA(cudaMemcpyAsync(k_val_orig_.get() + off, c->values, c->nnz * sizeof(double),
+                                cudaMemcpyHostToDevice, s));
+    }
+    off += c->nnz;
+  }
+  launch_check_cols(k_col_.get(), nnz_, int(n_), err.get(), s);
+  launch_check_rows(k_rp_.get(), k_col_.get(), int(m_), err.get(), s);
+  int herr = 0;
+  PDLP_CUDA(cudaMemcpyAsync(&herr, err.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  PDLP_CUDA(cudaStreamSynchronize(s));
+  if (herr & 1) invalid("csr: column index out of range");
+  if (herr & 2) invalid("csr: row_offsets must be nondecreasing");
+  if (herr & 4) invalid("csr: column indices must be strictly increasing within a row");
+
+  build_transpose();
+
+  // original vectors on the device (evaluation on the unscaled LP)
+  auto up = [&](DevBuf<double>& d, const std::vector<double>& h) {
+    d.alloc(h.size());
+    if (!h.empty())
+      PDLP_CUDA(cudaMemcpyAsync(d.get(), h.data(), h.size() * sizeof(double),
+                                cudaMemcpyHostToDevice, s));
+  };
+  up(c_orig_, c_);
+  up(l_orig_, l_);
+  up(u_orig_, u_);
+  up(q_orig_, q_);
+
+  precondition();
+
+  // tile plans (host planner over the offsets)
+  std::vector<int> rp_h(m_ + 1), rpt_h(n_ + 1);
+  PDLP_CUDA(cudaMemcpyAsync(rp_h.data(), k_rp_.get(), (m_ + 1) * sizeof(int),
+                            cudaMemcpyDeviceToHost, s));
+  PDLP_CUDA(cudaMemcpyAsync(rpt_h.data(), kt_rp_.get(), (n_ + 1) * sizeof(int),
+                            cudaMemcpyDeviceToHost, s));
+  PDLP_CUDA(cudaStreamSynchronize(s));
+  K_ = DevCsr{k_rp_.get(), k_col_.get(), k_val_.get(), k_val_orig_.get(), int(m_), int(n_), nnz_};
+  KT_ = DevCsr{kt_rp_.get(), kt_col_.get(), kt_val_.get(), kt_val_orig_.get(), int(n_), int(m_), nnz_};
+  k_plan_ = plan_tiles<int>(m_, rp_h.data(), parity(), kStreamMaxRow, kWarpMaxRow, kChunkNnz,
+                            kStreamNnz, kThreads);
+  kt_plan_ = plan_tiles<int>(n_, rpt_h.data(), parity(), kStreamMaxRow, kWarpMaxRow, kChunkNnz,
+                             kStreamNnz, kThreads);
+  plan(K_, rp_h, k_plan_.tiles, k_tiles_, k_chunk_, k_ctr_);
+  plan(KT_, rpt_h, kt_plan_.tiles, kt_tiles_, kt_chunk_, kt_ctr_);
+  K_.chunk_slots = k_plan_.chunk_slots;
+  KT_.chunk_slots = kt_plan_.chunk_slots;
+  {
+    // chunk counters sized by split rows
+    k_ctr_.alloc(std::max(1, k_plan_.split_rows));
+    k_ctr_.zero(s);
+    kt_ctr_.alloc(std::max(1, kt_plan_.split_rows));
+    kt_ctr_.zero(s);
+    K_.chunk_ctr = k_ctr_.get();
+    KT_.chunk_ctr = kt_ctr_.get();
+  }
+
+  allocate_iteration();
+  set_kernel_attributes();
+}
+
+void Solver::plan(DevCsr& a, const std::vector<int>&, std::vector<Tile>& tiles_host,
+                  DevBuf<Tile>& tiles, DevBuf<double>& chunk_part, DevBuf<unsigned>&) {
+  tiles.alloc(tiles_host.size());
+  PDLP_CUDA(cudaMemcpyAsync(tiles.get(), tiles_host.data(), tiles_host.size() * sizeof(Tile),
+                            cudaMemcpyHostToDevice, stream_));
+  int slots = 0;
+  for (const Tile& t : tiles_host)
+    if (t.kind == kTileChunk && t.nparts > 1) slots = std::max(slots, t.slot + t.nparts);
+  chunk_part.alloc(size_t(std::max(1, slots)) * 8);
+  a.tiles = tiles.get();
+  a.ntiles = int(tiles_host.size());
+  a.chunk_part = chunk_part.get();
+}
+
+// explicit_transpose (sparse_matrix.hpp:167-178) on the device: a stable LSD
+// radix sort of nnz ids by column keeps each column's entries in increasing
+// row order, i.e. the reference's CSR of K^T; integer output is exact.
+void Solver::build_transpose() {
+  cudaStream_t s = stream_;
+  kt_rp_.alloc(n_ + 1);
+  kt_col_.alloc(nnz_ + kVecPad);
+  kt_val_orig_.alloc(nnz_ + kVecPad);
+  kt_val_.alloc(nnz_ + kVecPad);
+  kt_col_.zero(s);
+  kt_val_orig_.zero(s);
+  kt_val_.zero(s);
+  const int nnz = int(nnz_);
+  DevBuf<int> row_of(nnz_), ids(nnz_), keys_out(nnz_), perm(nnz_), counts(n_ + 1);
+  launch_expand_rows(k_rp_.get(), int(m_), row_of.get(), s);
+  launch_iota(ids.get(), nnz_, s);
+  int end_bit = 1;
+  while ((int64_t(1) << end_bit) < n_) ++end_bit;
+  size_t tmp_bytes = 0;
+  PDLP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k_col_.get(), keys_out.get(),
+                                            ids.get(), perm.get(), nnz, 0, end_bit, s));
+  DevBuf<unsigned char> tmp(tmp_bytes);
+  PDLP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tmp_bytes, k_col_.get(), keys_out.get(),
+                                            ids.get(), perm.get(), nnz, 0, end_bit, s));
+  counts.zero(s);
+  launch_count_cols(k_col_.get(), nnz_, counts.get(), s);
+  size_t scan_bytes = 0;
+  PDLP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, counts.get(), kt_rp_.get(),
+                                          int(n_ + 1), s));
+  DevBuf<unsigned char> scan_tmp(scan_bytes);
+  PDLP_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp.get(), scan_bytes, counts.get(), kt_rp_.get(),
+                                          int(n_ + 1), s));
+  launch_gather_transpose(perm.get(), row_of.get(), k_val_orig_.get(), nnz_, kt_col_.get(),
+                          kt_val_orig_.get(), s);
+  PDLP_CUDA(cudaStreamSynchronize(s));
+}
+
+// make_scaling(vstack(G,A), mode, ruiz_iterations, alpha) (scaling.hpp:117-132)
+// then apply_scaling (scaling.hpp:137-170), all on the device.
+void Solver::precondition() {
+  cudaStream_t s = stream_;
+  d1_dev_.alloc(m_);
+  d2_dev_.alloc(n_);
+  launch_fill(d1_dev_.get(), m_, 1.0, s);
+  launch_fill(d2_dev_.get(), n_, 1.0, s);
+  DevBuf<double> rn(m_), cn(n_);
+  const int mode = params_.scaling;
+  if (mode != PDLP_SCALING_NONE) {
+    for (int it = 0; it < params_.ruiz_iterations; ++it) {  // ruiz_equilibrate :52-66
+      launch_row_absmax(k_rp_.get(), k_col_.get(), k_val_orig_.get(), int(m_), d1_dev_.get(),
+                        d2_dev_.get(), rn.get(), s);
+      launch_row_absmax(kt_rp_.get(), kt_col_.get(), kt_val_orig_.get(), int(n_), d2_dev_.get(),
+                        d1_dev_.get(), cn.get(), s);
+      launch_ruiz_update(d1_dev_.get(), rn.get(), int(m_), s);
+      launch_ruiz_update(d2_dev_.get(), cn.get(), int(n_), s);
+    }
+    if (mode == PDLP_SCALING_RUIZ_PC) {  // pock_chambolle_scale :72-94 + compose :98-112
+      const double alpha = params_.pock_chambolle_alpha;
+      launch_row_pnorm(k_rp_.get(), k_col_.get(), k_val_orig_.get(), int(m_), d1_dev_.get(),
+                       d2_dev_.get(), 2.0 - alpha, rn.get(), s);
+      launch_row_pnorm(kt_rp_.get(), kt_col_.get(), kt_val_orig_.get(), int(n_), d2_dev_.get(),
+                       d1_dev_.get(), alpha, cn.get(), s);
+      launch_pc_update(d1_dev_.get(), rn.get(), int(m_), 2.0 - alpha, s);
+      launch_pc_update(d2_dev_.get(), cn.get(), int(n_), alpha, s);
+    }
+  }
+  launch_scale_values(k_rp_.get(), k_col_.get(), k_val_orig_.get(), int(m_), d1_dev_.get(),
+                      d2_dev_.get(), k_val_.get(), s);
+  launch_scale_values(kt_rp_.get(), kt_col_.get(), kt_val_orig_.get(), int(n_), d2_dev_.get(),
+                      d1_dev_.get(), kt_val_.get(), s);
+  c_s_.alloc(n_);
+  l_s_.alloc(n_);
+  u_s_.alloc(n_);
+  q_s_.alloc(m_);
+  launch_scale_vectors(c_orig_.get(), l_orig_.get(), u_orig_.get(), q_orig_.get(), d1_dev_.get(),
+                       d2_dev_.get(), int(n_), int(m_), c_s_.get(), l_s_.get(), u_s_.get(),
+                       q_s_.get(), s);
+  // eta_hat_0 = 1 / max|K~| (solver.hpp:771-772): order-free max
+  const int nb = 296;
+  DevBuf<double> part(nb);
+  launch_block_absmax(k_val_.get(), nnz_, part.get(), nb, s);
+  std::vector<double> ph(nb);
+  d1_.resize(m_);
+  d2_.resize(n_);
+  PDLP_CUDA(cudaMemcpyAsync(ph.data(), part.get(), nb * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (m_)
+    PDLP_CUDA(cudaMemcpyAsync(d1_.data(), d1_dev_.get(), m_ * sizeof(double),
+                              cudaMemcpyDeviceToHost, s));
+  if (n_)
+    PDLP_CUDA(cudaMemcpyAsync(d2_.data(), d2_dev_.get(), n_ * sizeof(double),
+                              cudaMemcpyDeviceToHost, s));
+  PDLP_CUDA(cudaStreamSynchronize(s));
+  double mx = 0.0;
+  for (double v : ph) mx = std::max(mx, v);
+  eta_hat0_ = mx > 0.0 ? 1.0 / mx : 1.0;
+  // initialize_primal_weight on the scaled problem (solver.hpp:293-300, :774-776):
+  // the scaled vectors are the same products the device formed.
+  std::vector<double> cs(n_), qs(m_);
+  for (int64_t j = 0; j < n_; ++j) cs[j] = c_[j] * d2_[j];
+  for (int64_t i = 0; i < m_; ++i) qs[i] = q_[i] * d1_[i];
+  const double cn2 = seq_norm2(cs), qn2 = seq_norm2(qs);
+  const double w = (cn2 > params_.eps_zero && qn2 > params_.eps_zero) ? cn2 / qn2 : 1.0;
+  omega0_ = sclamp(w, params_.omega_min, params_.omega_max);
+}
+
+void Solver::allocate_iteration() {
+  cudaStream_t s = stream_;
+  for (auto& b : x_) b.alloc(n_);
+  for (auto& b : y_) b.alloc(m_);
+  for (auto& b : kx_) b.alloc(m_);
+  for (auto& b : kty_) b.alloc(n_);
+  avg_x_.alloc(n_);
+  avg_y_.alloc(m_);
+  x_start_.alloc(n_);
+  y_start_.alloc(m_);
+  const int avg_blocks = std::max<int64_t>(1, (m_ + 4095) / 4096);
+  const int p_grid = KT_.ntiles + avg_blocks;
+  d_part_.alloc(size_t(K_.ntiles) * 3);
+  p_part_.alloc(size_t(p_grid) * 2);
+  p_part_.zero(s);
+  const bool seq = parity();
+  seq_dy2_.alloc(seq ? m_ : 1);
+  seq_inter_.alloc(seq ? m_ : 1);
+  seq_dx2_.alloc(seq ? n_ : 1);
+  tab_cap_ = int(std::min<int64_t>(params_.evaluation_frequency, 4096));
+  red_tab_.alloc(tab_cap_);
+  gro_tab_.alloc(tab_cap_);
+  step_log_dev_.alloc(tab_cap_);
+  state_dev_.alloc(1);
+  state_dev_.zero(s);
+  hs_.alloc(1);
+  he_.alloc(1);
+  tab_host_.alloc(2 * size_t(tab_cap_));
+  log_host_.alloc(tab_cap_);
+  std::memset(hs_.get(), 0, sizeof(DevState));
+
+  DevIter& it = it_;
+  for (int i = 0; i < 3; ++i) {
+    it.x[i] = x_[i].get();
+    it.y[i] = y_[i].get();
+  }
+  for (int i = 0; i < 2; ++i) {
+    it.kx[i] = kx_[i].get();
+    it.kty[i] = kty_[i].get();
+  }
+  it.avg_x = avg_x_.get();
+  it.avg_y = avg_y_.get();
+  it.x_start = x_start_.get();
+  it.y_start = y_start_.get();
+  it.c = c_s_.get();
+  it.l = l_s_.get();
+  it.u = u_s_.get();
+  it.q = q_s_.get();
+  it.n = int(n_);
+  it.m = int(m_);
+  it.m1 = int(m1_);
+  it.p_grid = p_grid;
+  it.avg_blocks = avg_blocks;
+  it.d_part = d_part_.get();
+  it.p_part = p_part_.get();
+  it.seq_dy2 = seq_dy2_.get();
+  it.seq_inter = seq_inter_.get();
+  it.seq_dx2 = seq_dx2_.get();
+  it.red_tab = red_tab_.get();
+  it.gro_tab = gro_tab_.get();
+  it.step_log = step_log_dev_.get();
+  it.st = state_dev_.get();
+
+  X4_.alloc(size_t(n_) * 4);
+  Y4_.alloc(size_t(m_) * 4);
+  lam_.alloc(size_t(n_) * 4);
+  scratch_n_.alloc(n_);
+  const int grid0 = eval_grid0(int(n_), int(m_));
+  part0_.alloc(size_t(std::max(1, grid0)) * 4);
+  part1_.alloc(size_t(K_.ntiles) * 14);
+  part2_.alloc(size_t(KT_.ntiles) * 18);
+  seq_r_.alloc(seq ? size_t(m_) * 4 : 1);
+  seq_d_.alloc(seq ? size_t(n_) * 4 : 1);
+  eval_dev_.alloc(1);
+  DevEval& ev = ev_;
+  ev.X4 = X4_.get();
+  ev.Y4 = Y4_.get();
+  ev.lam = lam_.get();
+  ev.c = c_orig_.get();
+  ev.l = l_orig_.get();
+  ev.u = u_orig_.get();
+  ev.q = q_orig_.get();
+  ev.d1 = d1_dev_.get();
+  ev.d2 = d2_dev_.get();
+  ev.objective_constant = objective_constant_;
+  ev.part0 = part0_.get();
+  ev.part1 = part1_.get();
+  ev.part2 = part2_.get();
+  ev.grid0 = grid0;
+  ev.seq_r = seq_r_.get();
+  ev.seq_d = seq_d_.get();
+  ev.out = eval_dev_.get();
+}
+
+// The evaluation window as one CUDA graph: WHILE(cond) { dual; primal }, the
+// condition being cleared by the dual kernel's last CTA once the window's
+// accepted-step target is met (or the step failed).
+void Solver::capture_window_graph() {
+  PDLP_CUDA(cudaGraphCreate(&graph_, 0));
+  cudaGraphConditionalHandle h;
+  PDLP_CUDA(cudaGraphConditionalHandleCreate(&h, graph_, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  PDLP_CUDA(cudaGraphAddNode(&node, graph_, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  PDLP_CUDA(cudaStreamBeginCaptureToGraph(stream_, body, nullptr, nullptr, 0,
+                                          cudaStreamCaptureModeThreadLocal));
+  launch_dual(K_, it_, parity(), static_cast<unsigned long long>(h), 1, stream_);
+  launch_primal(KT_, it_, parity(), -1, stream_);
+  PDLP_CUDA(cudaStreamEndCapture(stream_, &body));
+  PDLP_CUDA(cudaGraphInstantiate(&graph_exec_, graph_, 0));
+  cond_handle_ = static_cast<unsigned long long>(h);
+}
+
+void Solver::upload_state() {
+  PDLP_CUDA(cudaMemcpyAsync(state_dev_.get(), hs_.get(), sizeof(DevState), cudaMemcpyHostToDevice,
+                            stream_));
+}
+
+void Solver::download_state() {
+  PDLP_CUDA(cudaMemcpyAsync(hs_.get(), state_dev_.get(), sizeof(DevState), cudaMemcpyDeviceToHost,
+                            stream_));
+  PDLP_CUDA(cudaStreamSynchronize(stream_));
+}
+
+double Solver::elapsed() const {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0_).count();
+}
+
+// ---------------------------------------------------------------------------
+// the loop
+// ---------------------------------------------------------------------------
+
+void Solver::iterate_begin(int32_t* status) {
+  t0_ = std::chrono::steady_clock::now();
+  DevState& st = *hs_.get();
+  std::memset(&st, 0, sizeof st);
+  st.eta = eta_hat0_;
+  st.eta_acc = eta_hat0_;
+  st.omega = omega0_;
+  st.ix_cur = 0, st.ix_prev = 1, st.ix_trial = 2;
+  st.iy_cur = 0, st.iy_prev = 1, st.iy_trial = 2;
+  st.ikx_cur = 0, st.ikty_cur = 0;
+  st.record_log = params_.record_step_log ? 1 : 0;
+  outer_ = 0;
+  launches_ = 0;
+  evaluations_ = 0;
+  step_log_.clear();
+  restart_log_.clear();
+  finished_ = false;
+  begun_ = true;
+  state_valid_ = true;
+  std::memset(&info_, 0, sizeof info_);
+  upload_state();
+  launch_zero_iterate(it_, stream_);  // z = 0, Kx = K 0 = 0, K'y = 0 (solver.hpp:764-769)
+  ++launches_;
+  // initial evaluation on the unscaled zero point (solver.hpp:784-792)
+  evaluate();
+  const KktHost r0 = kkt(0);
+  kkt_epoch_start_ = r0.weighted(st.omega);
+  kkt_last_ = kkt_epoch_start_;
+  if (terminated(r0)) {
+    finish(PDLP_STATUS_OPTIMAL, 0, 0, 0, r0);
+  } else {
+    // first trial x' = proj(x - tau (c - K'y)) at z = 0
+    upload_state();
+    launch_primal(KT_, it_, parity(), kPRetry, stream_);
+    ++launches_;
+  }
+  if (status) *status = finished_ ? info_.status : PDLP_STATUS_RUNNING;
+}
+
+void Solver::iterate_run(int64_t count, int32_t* status) {
+  if (!begun_ || !state_valid_) throw std::logic_error("iterate_run before iterate_begin");
+  DevState& st = *hs_.get();
+  const int64_t freq = params_.evaluation_frequency;
+  int64_t done = 0;
+  while (!finished_ && done < count) {
+    // limits at the loop top (solver.hpp:795-804); the time limit is checked
+    // once per window
+    if (st.total >= params_.iteration_limit) {
+      evaluate();
+      finish_candidate(PDLP_STATUS_ITERATION_LIMIT);
+      break;
+    }
+    if (elapsed() >= params_.time_limit_seconds) {
+      evaluate();
+      finish_candidate(PDLP_STATUS_TIME_LIMIT);
+      break;
+    }
+    int64_t target = freq - st.inner % freq;
+    target = std::min<int64_t>(target, params_.iteration_limit - st.total);
+    target = std::min<int64_t>(target, count - done);
+    target = std::min<int64_t>(target, tab_cap_);
+    const int64_t before = st.total;
+    run_window(int(target));
+    done += st.total - before;
+    if (st.failure) {
+      evaluate();
+      finish_candidate(PDLP_STATUS_NUMERICAL_ERROR,
+                       "non-finite iterate in adaptive step at iteration " + std::to_string(st.total));
+      break;
+    }
+    if (st.inner % freq != 0) continue;
+    evaluate();
+    evaluation_block();
+  }
+  if (status) *status = finished_ ? info_.status : PDLP_STATUS_RUNNING;
+}
+
+void Solver::run_window(int target) {
+  DevState& st = *hs_.get();
+  double* red = tab_host_.get();
+  double* gro = red + tab_cap_;
+  for (int i = 0; i < target; ++i) {
+    // factors of adaptive_step_cached for step counter k = total + 1 (solver.hpp:388-390)
+    const double kp1 = double(st.total + 1 + i) + 1.0;
+    red[i] = 1.0 - std::pow(kp1, -params_.step_reduction_exponent);
+    gro[i] = 1.0 + std::pow(kp1, -params_.step_growth_exponent);
+  }
+  st.window_target = target;
+  st.window_accepts = 0;
+  st.table_base = st.total;
+  st.failure = 0;
+  const int64_t trials_before = st.trials_total;
+  PDLP_CUDA(cudaMemcpyAsync(red_tab_.get(), red, target * sizeof(double), cudaMemcpyHostToDevice,
+                            stream_));
+  PDLP_CUDA(cudaMemcpyAsync(gro_tab_.get(), gro, target * sizeof(double), cudaMemcpyHostToDevice,
+                            stream_));
+  upload_state();
+  if (params_.use_cuda_graph) {
+    if (!graph_exec_) capture_window_graph();
+    PDLP_CUDA(cudaGraphLaunch(graph_exec_, stream_));
+    download_state();
+  } else {
+    int remaining = target;
+    while (true) {
+      for (int i = 0; i < remaining; ++i) {
+        launch_dual(K_, it_, parity(), 0, 0, stream_);
+        launch_primal(KT_, it_, parity(), -1, stream_);
+      }
+      download_state();
+      if (st.failure || st.window_accepts >= target) break;
+      remaining = target - st.window_accepts;
+    }
+  }
+  launches_ += 2 * (st.trials_total - trials_before);
+  if (st.record_log && st.window_accepts > 0) {
+    PDLP_CUDA(cudaMemcpyAsync(log_host_.get(), step_log_dev_.get(),
+                              st.window_accepts * sizeof(pdlp_step_log_entry),
+                              cudaMemcpyDeviceToHost, stream_));
+    PDLP_CUDA(cudaStreamSynchronize(stream_));
+    step_log_.insert(step_log_.end(), log_host_.get(), log_host_.get() + st.window_accepts);
+  }
+}
+
+void Solver::evaluate() {
+  upload_state();
+  launch_eval(K_, KT_, it_, ev_, parity(), stream_);
+  launches_ += parity() ? 5 : 4;
+  ++evaluations_;
+  PDLP_CUDA(cudaMemcpyAsync(he_.get(), eval_dev_.get(), sizeof(EvalOut), cudaMemcpyDeviceToHost,
+                            stream_));
+  PDLP_CUDA(cudaStreamSynchronize(stream_));
+}
+
+KktHost Solver::kkt(int slot) const {
+  const EvalOut& e = *he_.get();
+  return KktHost{e.prn[slot], e.drn[slot], e.pobj[slot], e.dobj[slot]};
+}
+
+// termination_criteria_met (solver.hpp:204-222)
+bool Solver::terminated(const KktHost& r) const {
+  if (!std::isfinite(r.prn) || !std::isfinite(r.drn) || !std::isfinite(r.pobj) ||
+      !std::isfinite(r.dobj))
+    return false;
+  const double eps = params_.eps_optimal;
+  const bool gap_ok = std::abs(r.gap()) <= eps * (1.0 + std::abs(r.dobj) + std::abs(r.pobj));
+  const bool p_ok = r.prn <= eps * (1.0 + rhs_norm_);
+  const bool d_ok = r.drn <= eps * (1.0 + obj_norm_);
+  return gap_ok && p_ok && d_ok;
+}
+
+// The evaluation block of SolveLoop::run (solver.hpp:843-927).
+void Solver::evaluation_block() {
+  DevState& st = *hs_.get();
+  const EvalOut& e = *he_.get();
+  const KktHost cur = kkt(0), avg = kkt(1);
+  const double kc = cur.weighted(st.omega), ka = avg.weighted(st.omega);
+  const int cand = !(kc < ka) ? 1 : 0;  // ties go to the average (:718)
+  const KktHost rc = cand ? avg : cur, ro = cand ? cur : avg;
+  const double kkt_cand = cand ? ka : kc;
+  if (terminated(rc)) return finish(PDLP_STATUS_OPTIMAL, cand, cand, cand, rc);
+  if (terminated(ro)) return finish(PDLP_STATUS_OPTIMAL, 1 - cand, 1 - cand, 1 - cand, ro);
+
+  // check_infeasibility: delta ray, then normalized ray (solver.hpp:581-590)
+  const double eps_inf = params_.eps_infeasible, eps_zero = params_.eps_zero;
+  for (int r = 0; r < 2; ++r) {
+    const double yn = e.y_norm[r];
+    if (yn > eps_zero && e.kty_resid[r] <= eps_inf * yn && e.ray_dobj[r] > eps_inf * yn) {
+      finish(PDLP_STATUS_PRIMAL_INFEASIBLE, -1, 2 + r, 2 + r, rc);
+      info_.has_certificate = 1;
+      return;
+    }
+    const double xn = e.x_norm[r];
+    if (xn > eps_zero) {
+      const double tol = eps_inf * xn;
+      const bool ok = e.ax_norm[r] <= tol && !(e.gx_negmax[r] > tol) && !(e.xl_negmax[r] > tol) &&
+                      !(e.xu_max[r] > tol) && e.cx[r] < -tol;
+      if (ok) {
+        finish(PDLP_STATUS_DUAL_INFEASIBLE, 2 + r, -1, -2, rc);
+        info_.has_certificate = 1;
+        return;
+      }
+    }
+  }
+
+  // should_restart (solver.hpp:270-286, :887-892)
+  const double prev = kkt_last_;
+  int crit = PDLP_RESTART_NONE;
+  if (kkt_cand <= params_.beta_sufficient * kkt_epoch_start_)
+    crit = PDLP_RESTART_SUFFICIENT_DECAY;
+  else if (kkt_cand <= params_.beta_necessary * kkt_epoch_start_ && kkt_cand > prev)
+    crit = PDLP_RESTART_NECESSARY_DECAY;
+  else if (double(st.inner) >= params_.beta_artificial * double(st.total))
+    crit = PDLP_RESTART_LONG_INNER_LOOP;
+  kkt_last_ = kkt_cand;
+  if (crit == PDLP_RESTART_NONE) return;
+
+  pdlp_restart_event ev{};
+  ev.total_iterations = st.total;
+  ev.epoch_length = st.inner;
+  ev.criterion = crit;
+  ev.candidate_is_average = cand;
+  ev.kkt_candidate = kkt_cand;
+  ev.kkt_previous_candidate = prev;
+  ev.kkt_epoch_start = kkt_epoch_start_;
+  ev.omega_before = st.omega;
+
+  // restart (solver.hpp:907-927): z_start = z = candidate, fresh products,
+  // averages reset, primal weight update (:305-325) with host glibc exp/log
+  const double dx = std::sqrt(e.dx2[cand]), dy = std::sqrt(e.dy2[cand]);
+  double omega = st.omega;
+  if (dx > eps_zero && dy > eps_zero)
+    omega = std::exp(params_.theta_smoothing * std::log(dy / dx) +
+                     (1.0 - params_.theta_smoothing) * std::log(st.omega));
+  const bool from_avg = cand == 1 && st.wsum != 0.0;
+  upload_state();
+  launch_restart_copy(it_, from_avg ? 1 : 0, stream_);
+  st.omega = sclamp(omega, params_.omega_min, params_.omega_max);
+  st.wsum = 0.0;
+  st.inner = 0;
+  outer_ += 1;
+  upload_state();
+  launch_spmv(K_, false, it_.x[st.ix_cur], it_.kx[st.ikx_cur], parity(), stream_);
+  launch_primal(KT_, it_, parity(), kPRestart, stream_);
+  launches_ += 3;
+  ev.omega_after = st.omega;
+  restart_log_.push_back(ev);
+  kkt_epoch_start_ = rc.weighted(st.omega);
+  kkt_last_ = kkt_epoch_start_;
+}
+
+void Solver::finish_candidate(int status, const std::string& msg) {
+  const DevState& st = *hs_.get();
+  const KktHost cur = kkt(0), avg = kkt(1);
+  const int cand = !(cur.weighted(st.omega) < avg.weighted(st.omega)) ? 1 : 0;
+  finish(status, cand, cand, cand, cand ? avg : cur, msg);
+}
+
+// SolveLoop::finish (solver.hpp:741-757). slot_x/slot_y: which of the four
+// evaluated points supplies x / y (-1 = zero vector); slot_lam: reduced costs
+// of that slot, or -2 for reduced_costs(lp, 0) of a dual-infeasibility exit.
+void Solver::finish(int status, int slot_x, int slot_y, int slot_lam, const KktHost& r,
+                    const std::string& msg) {
+  const DevState& st = *hs_.get();
+  cudaStream_t s = stream_;
+  rx_.assign(n_, 0.0);
+  ry_.assign(m_, 0.0);
+  rlam_.assign(n_, 0.0);
+  if (slot_x >= 0 && n_)
+    PDLP_CUDA(cudaMemcpy2DAsync(rx_.data(), sizeof(double), X4_.get() + slot_x, 4 * sizeof(double),
+                                sizeof(double), n_, cudaMemcpyDeviceToHost, s));
+  if (slot_y >= 0 && m_)
+    PDLP_CUDA(cudaMemcpy2DAsync(ry_.data(), sizeof(double), Y4_.get() + slot_y, 4 * sizeof(double),
+                                sizeof(double), m_, cudaMemcpyDeviceToHost, s));
+  if (n_) {
+    if (slot_lam >= 0) {
+      PDLP_CUDA(cudaMemcpyAsync(rlam_.data(), lam_.get() + size_t(slot_lam) * n_,
+                                n_ * sizeof(double), cudaMemcpyDeviceToHost, s));
+    } else {
+      launch_reduced_of_objective(c_orig_.get(), l_orig_.get(), u_orig_.get(), int(n_),
+                                  scratch_n_.get(), s);
+      PDLP_CUDA(cudaMemcpyAsync(rlam_.data(), scratch_n_.get(), n_ * sizeof(double),
+                                cudaMemcpyDeviceToHost, s));
+    }
+  }
+  PDLP_CUDA(cudaStreamSynchronize(s));
+  pdlp_result_info& in = info_;
+  std::memset(&in, 0, sizeof in);
+  in.status = status;
+  in.primal_objective_raw = r.pobj;
+  in.dual_objective_raw = r.dobj;
+  in.primal_objective = r.pobj + objective_constant_;
+  in.dual_objective = r.dobj + objective_constant_;
+  in.gap_abs = std::abs(r.gap());
+  in.primal_residual_norm = r.prn;
+  in.dual_residual_norm = r.drn;
+  in.relative_gap = in.gap_abs / (1.0 + std::abs(r.dobj) + std::abs(r.pobj));
+  in.relative_primal_residual = r.prn / (1.0 + rhs_norm_);
+  in.relative_dual_residual = r.drn / (1.0 + obj_norm_);
+  in.kkt_omega = r.weighted(st.omega);
+  in.iterations = st.total;
+  in.restarts = outer_;
+  in.solve_seconds = elapsed();
+  in.setup_seconds = setup_seconds_;
+  in.step_log_size = int64_t(step_log_.size());
+  in.restart_log_size = int64_t(restart_log_.size());
+  in.num_variables = n_;
+  in.num_constraints = m_;
+  in.trials = st.trials_total;
+  in.evaluations = evaluations_;
+  in.gpu_launches = launches_;
+  std::snprintf(in.message, sizeof in.message, "%s", msg.c_str());
+  finished_ = true;
+}
+
+void Solver::solve(pdlp_result_info* info) {
+  int32_t status;
+  iterate_begin(&status);
+  while (!finished_) iterate_run(std::numeric_limits<int64_t>::max(), &status);
+  if (info) *info = info_;
+}
+
+// ---------------------------------------------------------------------------
+// accessors
+// ---------------------------------------------------------------------------
+
+void Solver::get_iterate(double* x, double* y, double* kx, double* kty, int64_t* counters,
+                         double* scalars) {
+  if (!state_valid_) throw std::logic_error("no live iterate (call iterate_begin)");
+  const DevState& st = *hs_.get();
+  cudaStream_t s = stream_;
+  if (x && n_) PDLP_CUDA(cudaMemcpyAsync(x, x_[st.ix_cur].get(), n_ * 8, cudaMemcpyDeviceToHost, s));
+  if (y && m_) PDLP_CUDA(cudaMemcpyAsync(y, y_[st.iy_cur].get(), m_ * 8, cudaMemcpyDeviceToHost, s));
+  if (kx && m_)
+    PDLP_CUDA(cudaMemcpyAsync(kx, kx_[st.ikx_cur].get(), m_ * 8, cudaMemcpyDeviceToHost, s));
+  if (kty && n_)
+    PDLP_CUDA(cudaMemcpyAsync(kty, kty_[st.ikty_cur].get(), n_ * 8, cudaMemcpyDeviceToHost, s));
+  PDLP_CUDA(cudaStreamSynchronize(s));
+  if (counters) {
+    counters[0] = st.total;
+    counters[1] = st.inner;
+    counters[2] = outer_;
+    counters[3] = st.trials_total;
+  }
+  if (scalars) {
+    scalars[0] = st.eta_acc;
+    scalars[1] = st.eta;
+    scalars[2] = st.omega;
+    scalars[3] = st.wsum;
+  }
+}
+
+void Solver::get_solution(double* x, double* y, double* lambda, double* lambda_pos,
+                          double* lambda_neg) {
+  if (!finished_) throw std::logic_error("no solution: solve has not finished");
+  if (x) std::copy(rx_.begin(), rx_.end(), x);
+  if (y) std::copy(ry_.begin(), ry_.end(), y);
+  for (int64_t j = 0; j < n_; ++j) {
+    const double v = rlam_[j];
+    if (lambda) lambda[j] = v;
+    if (lambda_pos) lambda_pos[j] = v > 0.0 ? v : 0.0;
+    if (lambda_neg) lambda_neg[j] = v < 0.0 ? -v : 0.0;
+  }
+}
+
+int64_t Solver::get_step_log(pdlp_step_log_entry* out, int64_t cap) const {
+  const int64_t k = std::min<int64_t>(cap, int64_t(step_log_.size()));
+  if (out) std::copy(step_log_.begin(), step_log_.begin() + k, out);
+  return k;
+}
+
+int64_t Solver::get_restart_log(pdlp_restart_event* out, int64_t cap) const {
+  const int64_t k = std::min<int64_t>(cap, int64_t(restart_log_.size()));
+  if (out) std::copy(restart_log_.begin(), restart_log_.begin() + k, out);
+  return k;
+}
+
+void Solver::get_scaling(double* row_scale, double* col_scale) const {
+  if (row_scale) std::copy(d1_.begin(), d1_.end(), row_scale);
+  if (col_scale) std::copy(d2_.begin(), d2_.end(), col_scale);
+}
+
+void Solver::spmv(int op, const double* in, double* out) {
+  const bool transpose = op == PDLP_OP_KT_SCALED || op == PDLP_OP_KT_ORIGINAL;
+  const bool orig = op == PDLP_OP_K_ORIGINAL || op == PDLP_OP_KT_ORIGINAL;
+  if (op < 0 || op > 3) invalid("spmv: unknown operator");
+  const int64_t nin = transpose ? m_ : n_, nout = transpose ? n_ : m_;
+  DevBuf<double> din(nin), dout(nout);
+  if (nin) PDLP_CUDA(cudaMemcpyAsync(din.get(), in, nin * 8, cudaMemcpyHostToDevice, stream_));
+  launch_spmv(transpose ? KT_ : K_, orig, din.get(), dout.get(), parity(), stream_);
+  if (nout) PDLP_CUDA(cudaMemcpyAsync(out, dout.get(), nout * 8, cudaMemcpyDeviceToHost, stream_));
+  PDLP_CUDA(cudaStreamSynchronize(stream_));
+}
+
+// Times the fused iteration kernels on a live window (after a solve). Each
+// repetition runs a real trial (dual then primal); the events bracket only the
+// kernel being timed. Leaves the iterate state invalid.
+void Solver::time_kernel(int which, int reps, double* avg_ms, double* bytes) {
+  if (!begun_) {
+    int32_t s;
+    iterate_begin(&s);
+  }
+  reps = std::max(1, std::min(reps, tab_cap_));
+  DevState& st = *hs_.get();
+  st.failure = 0;
+  st.window_accepts = 0;
+  st.window_target = 1 << 30;
+  st.table_base = st.total;
+  st.record_log = 0;
+  double* red = tab_host_.get();
+  double* gro = red + tab_cap_;
+  for (int i = 0; i < reps; ++i) {
+    const double kp1 = double(st.total + 1 + i) + 1.0;
+    red[i] = 1.0 - std::pow(kp1, -params_.step_reduction_exponent);
+    gro[i] = 1.0 + std::pow(kp1, -params_.step_growth_exponent);
+  }
+  PDLP_CUDA(cudaMemcpyAsync(red_tab_.get(), red, reps * 8, cudaMemcpyHostToDevice, stream_));
+  PDLP_CUDA(cudaMemcpyAsync(gro_tab_.get(), gro, reps * 8, cudaMemcpyHostToDevice, stream_));
+  upload_state();
+  // a trial needs a fresh x'; recompute it from the current point
+  launch_primal(KT_, it_, parity(), kPRetry, stream_);
+  std::vector<cudaEvent_t> ev(2 * reps);
+  for (auto& e : ev) PDLP_CUDA(cudaEventCreate(&e));
+  for (int r = 0; r < reps; ++r) {
+    if (which == 0) PDLP_CUDA(cudaEventRecord(ev[2 * r], stream_));
+    launch_dual(K_, it_, parity(), 0, 0, stream_);
+    if (which == 0) PDLP_CUDA(cudaEventRecord(ev[2 * r + 1], stream_));
+    if (which == 1) PDLP_CUDA(cudaEventRecord(ev[2 * r], stream_));
+    launch_primal(KT_, it_, parity(), -1, stream_);
+    if (which == 1) PDLP_CUDA(cudaEventRecord(ev[2 * r + 1], stream_));
+  }
+  PDLP_CUDA(cudaStreamSynchronize(stream_));
+  double total = 0.0;
+  for (int r = 0; r < reps; ++r) {
+    float ms = 0.f;
+    PDLP_CUDA(cudaEventElapsedTime(&ms, ev[2 * r], ev[2 * r + 1]));
+    total += ms;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  download_state();
+  state_valid_ = false;
+  if (avg_ms) *avg_ms = total / reps;
+  const double nnz = double(nnz_), n = double(n_), m = double(m_);
+  if (bytes) {
+    // algorithmic bytes of one launch: int32 index + fp64
+    // value per nonzero, int32 offsets, each dense stream touched once
+    if (which == 0)
+      *bytes = 12.0 * nnz + 4.0 * (m + 1) + 8.0 * n + 8.0 * 5.0 * m;
+    else
+      *bytes = 12.0 * nnz + 4.0 * (n + 1) + 8.0 * m + 8.0 * 8.0 * n + 8.0 * 3.0 * m;
+  }
+}
+
+void Solver::sizes(int64_t* out) const {
+  out[0] = n_;
+  out[1] = m_;
+  out[2] = m1_;
+  out[3] = nnz_;
+}
+
+}  // namespace pdlp

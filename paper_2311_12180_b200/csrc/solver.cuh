@@ -1,0 +1,177 @@
+// solver.cuh — host runtime of the B200 restarted-PDHG solver (one handle).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <string>
+#include <vector>
+
+#include "../../include/pdlp_b200.h"
+#include "common.cuh"
+#include "device_state.h"
+#include "tiles.h"
+
+namespace pdlp {
+
+template <class T>
+class DevBuf {
+ public:
+  DevBuf() = default;
+  explicit DevBuf(size_t n) { alloc(n); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p_ = o.p_;
+      n_ = o.n_;
+      o.p_ = nullptr;
+      o.n_ = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(size_t n) {
+    release();
+    n_ = n;
+    PDLP_CUDA(cudaMalloc(&p_, (n ? n : 1) * sizeof(T)));
+  }
+  void zero(cudaStream_t s) { PDLP_CUDA(cudaMemsetAsync(p_, 0, (n_ ? n_ : 1) * sizeof(T), s)); }
+  T* get() const { return p_; }
+  size_t size() const { return n_; }
+
+ private:
+  void release() {
+    if (p_) cudaFree(p_);
+    p_ = nullptr;
+  }
+  T* p_ = nullptr;
+  size_t n_ = 0;
+};
+
+template <class T>
+class PinnedBuf {
+ public:
+  PinnedBuf() = default;
+  PinnedBuf(const PinnedBuf&) = delete;
+  PinnedBuf& operator=(const PinnedBuf&) = delete;
+  ~PinnedBuf() {
+    if (p_) cudaFreeHost(p_);
+  }
+  void alloc(size_t n) {
+    if (p_) cudaFreeHost(p_);
+    PDLP_CUDA(cudaMallocHost(&p_, (n ? n : 1) * sizeof(T)));
+    n_ = n;
+  }
+  T* get() const { return p_; }
+  T& operator[](size_t i) const { return p_[i]; }
+
+ private:
+  T* p_ = nullptr;
+  size_t n_ = 0;
+};
+
+struct KktHost {  // KktResiduals (solver.hpp:109-123)
+  double prn, drn, pobj, dobj;
+  double gap() const { return dobj - pobj; }
+  double weighted(double omega) const;
+};
+
+class Solver {
+ public:
+  Solver(const pdlp_lp& lp, const pdlp_params& params);
+  ~Solver();
+
+  void solve(pdlp_result_info* info);
+  void iterate_begin(int32_t* status);
+  void iterate_run(int64_t n, int32_t* status);
+  void get_iterate(double* x, double* y, double* kx, double* kty, int64_t* counters,
+                   double* scalars);
+  void get_solution(double* x, double* y, double* lambda, double* lambda_pos, double* lambda_neg);
+  int64_t get_step_log(pdlp_step_log_entry* out, int64_t cap) const;
+  int64_t get_restart_log(pdlp_restart_event* out, int64_t cap) const;
+  void get_scaling(double* row_scale, double* col_scale) const;
+  void spmv(int op, const double* in, double* out);
+  void time_kernel(int which, int reps, double* avg_ms, double* bytes);
+  void sizes(int64_t* out) const;
+  const pdlp_result_info& info() const { return info_; }
+
+ private:
+  void setup(const pdlp_lp& lp);
+  void build_transpose();
+  void precondition();
+  void plan(DevCsr& a, const std::vector<int>& rp_host, std::vector<Tile>& tiles_host,
+            DevBuf<Tile>& tiles, DevBuf<double>& chunk_part, DevBuf<unsigned>& chunk_ctr);
+  void allocate_iteration();
+  void capture_window_graph();
+  void upload_state();
+  void download_state();
+  void run_window(int target);
+  void evaluate();
+  KktHost kkt(int slot) const;
+  bool terminated(const KktHost& r) const;
+  void evaluation_block();
+  void finish(int status, int slot_x, int slot_y, int slot_lam, const KktHost& r,
+              const std::string& msg = {});
+  void finish_candidate(int status, const std::string& msg = {});
+  double elapsed() const;
+  bool parity() const { return params_.mode == PDLP_MODE_PARITY; }
+
+  pdlp_params params_;
+  cudaStream_t stream_ = nullptr;
+  int64_t n_ = 0, m_ = 0, m1_ = 0, m2_ = 0, nnz_ = 0;
+  double objective_constant_ = 0.0;
+
+  // host copies of the original vectors (evaluation bookkeeping is host-side)
+  std::vector<double> c_, q_, l_, u_, d1_, d2_;
+  double rhs_norm_ = 0.0, obj_norm_ = 0.0;  // termination_norms (solver.hpp:157-163)
+  double eta_hat0_ = 1.0, omega0_ = 1.0;
+
+  // operator storage: K = (G; A) and its separately stored transpose
+  DevBuf<int> k_rp_, k_col_, kt_rp_, kt_col_;
+  DevBuf<double> k_val_, k_val_orig_, kt_val_, kt_val_orig_;
+  DevBuf<Tile> k_tiles_, kt_tiles_;
+  DevBuf<double> k_chunk_, kt_chunk_;
+  DevBuf<unsigned> k_ctr_, kt_ctr_;
+  TilePlan k_plan_, kt_plan_;
+  DevCsr K_{}, KT_{};
+
+  // vectors
+  DevBuf<double> c_orig_, l_orig_, u_orig_, q_orig_, d1_dev_, d2_dev_;
+  DevBuf<double> c_s_, l_s_, u_s_, q_s_;
+  DevBuf<double> x_[3], y_[3], kx_[2], kty_[2], avg_x_, avg_y_, x_start_, y_start_;
+  DevBuf<double> d_part_, p_part_, seq_dy2_, seq_inter_, seq_dx2_;
+  DevBuf<double> red_tab_, gro_tab_;
+  DevBuf<pdlp_step_log_entry> step_log_dev_;
+  DevBuf<DevState> state_dev_;
+  DevBuf<double> X4_, Y4_, lam_, part0_, part1_, part2_, seq_r_, seq_d_, scratch_n_, scratch_m_;
+  DevBuf<EvalOut> eval_dev_;
+  DevIter it_{};
+  DevEval ev_{};
+  int tab_cap_ = 0;
+
+  PinnedBuf<DevState> hs_;
+  PinnedBuf<EvalOut> he_;
+  PinnedBuf<double> tab_host_;
+  PinnedBuf<pdlp_step_log_entry> log_host_;
+
+  cudaGraph_t graph_ = nullptr;
+  cudaGraphExec_t graph_exec_ = nullptr;
+  unsigned long long cond_handle_ = 0;
+
+  // host-side loop state (solver.hpp:683-698)
+  int64_t outer_ = 0;
+  double kkt_epoch_start_ = 0.0, kkt_last_ = 0.0;
+  std::chrono::steady_clock::time_point t0_;
+  bool begun_ = false, finished_ = false, state_valid_ = false;
+  int64_t launches_ = 0, evaluations_ = 0;
+  double setup_seconds_ = 0.0;
+  std::vector<pdlp_step_log_entry> step_log_;
+  std::vector<pdlp_restart_event> restart_log_;
+  pdlp_result_info info_{};
+  std::vector<double> rx_, ry_, rlam_;
+};
+
+}  // namespace pdlp

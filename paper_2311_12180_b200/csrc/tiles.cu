@@ -1,0 +1,56 @@
+// tiles.cu — host-side tile planner (see tiles.h).
+#include <algorithm>
+
+#include "tiles.h"
+
+namespace pdlp {
+
+template <class Off>
+TilePlan plan_tiles(int64_t rows, const Off* rp, bool parity, int stream_max_row,
+                    int warp_max_row, int chunk_nnz, int stream_nnz, int threads) {
+  TilePlan plan;
+  int64_t r = 0;
+  auto len = [&](int64_t i) { return int64_t(rp[i + 1] - rp[i]); };
+  while (r < rows) {
+    const int64_t l = len(r);
+    if (l <= stream_max_row) {
+      const int64_t r0 = r, k0 = rp[r];
+      while (r < rows && r - r0 < threads && len(r) <= stream_max_row &&
+             int64_t(rp[r + 1]) - k0 <= stream_nnz)
+        ++r;
+      plan.tiles.push_back({kTileStream, int32_t(r0), int32_t(r), int32_t(k0), int32_t(rp[r]), 0, 1, 0});
+      ++plan.stream_tiles;
+    } else if (!parity && l <= warp_max_row) {
+      const int64_t r0 = r;
+      const int warps = threads / 32;
+      while (r < rows && r - r0 < warps && len(r) > stream_max_row && len(r) <= warp_max_row) ++r;
+      plan.tiles.push_back({kTileWarp, int32_t(r0), int32_t(r), int32_t(rp[r0]), int32_t(rp[r]), 0, 1, 0});
+      ++plan.warp_tiles;
+    } else {
+      const int64_t k0 = rp[r], k1 = rp[r + 1];
+      const int64_t parts = parity ? 1 : std::max<int64_t>(1, (l + chunk_nnz - 1) / chunk_nnz);
+      const int32_t ctr = parts > 1 ? plan.split_rows++ : -1;
+      for (int64_t p = 0; p < parts; ++p) {
+        const int64_t a = k0 + p * chunk_nnz;
+        const int64_t b = parts == 1 ? k1 : std::min<int64_t>(k1, a + chunk_nnz);
+        plan.tiles.push_back({kTileChunk, int32_t(r), ctr, int32_t(a), int32_t(b), int32_t(p),
+                              int32_t(parts), plan.chunk_slots});
+        ++plan.chunk_tiles;
+      }
+      if (parts > 1) plan.chunk_slots += int32_t(parts);
+      ++r;
+    }
+  }
+  // Degenerate operators (no rows) still get one empty tile, so every fused
+  // kernel has a CTA to run its reductions and step decision.
+  if (plan.tiles.empty()) {
+    plan.tiles.push_back({kTileStream, 0, 0, 0, 0, 0, 1, 0});
+    ++plan.stream_tiles;
+  }
+  return plan;
+}
+
+template TilePlan plan_tiles<int>(int64_t, const int*, bool, int, int, int, int, int);
+template TilePlan plan_tiles<int64_t>(int64_t, const int64_t*, bool, int, int, int, int, int);
+
+}  // namespace pdlp
