@@ -143,6 +143,7 @@ typedef struct {
   int64_t restarts;
   double solve_seconds;  /* loop time, excludes setup like the reference (:636-646,760) */
   double setup_seconds;  /* upload + K^T build + preconditioning (B200 extension) */
+  double device_seconds; /* solve loop timed with CUDA events on the solver's stream */
   double primal_objective;
   double dual_objective;
   double primal_objective_raw;

@@ -64,6 +64,7 @@ def load(kind: str = "oracle") -> C.CDLL:
         "from_triplets": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, i64p, i64p, dp, i64p, i64p,
                                     dp, i64p]),
         "last_error": (C.c_char_p, []),
+        "check_termination": (C.c_int, [LPP, dp, dp, C.c_double, dp]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(lib, p + name)
@@ -208,6 +209,18 @@ def from_triplets(rows: int, cols: int, r, c, v, kind: str = "oracle") -> CsrMat
                                                     abi.dptr(val), C.byref(nnz)))
     k = nnz.value
     return CsrMatrix(rows, cols, off, col[:k].copy(), val[:k].copy())
+
+
+def check_termination(lp: GeneralFormLp, x, y, eps: float, kind: str = "oracle") -> dict:
+    """The reference's own criteria recomputed at a returned point (criterion 2 style)."""
+    lib = load(kind)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    out = np.zeros(5)
+    lpa = lp.to_abi()
+    _err(lib, kind, _f(lib, kind, "check_termination")(C.byref(lpa), abi.dptr(x), abi.dptr(y), eps, abi.dptr(out)))
+    return {"terminated": bool(out[0]), "primal_residual_norm": out[1], "dual_residual_norm": out[2],
+            "primal_objective_raw": out[3], "dual_objective_raw": out[4]}
 
 
 def read_mps(path: str | os.PathLike) -> GeneralFormLp:

@@ -1276,6 +1276,28 @@ int oracle_transpose(const pdlp_csr* a, int64_t* off, int64_t* col, double* val)
   return rc;
 }
 
+int oracle_check_termination(const pdlp_lp* lpin, const double* x, const double* y, double eps,
+                             double* out) {
+  lp_t lp;
+  int rc = lp_from_abi(lpin, &lp);
+  if (rc) {
+    lp_free(&lp);
+    return rc;
+  }
+  term_norms_t nn;
+  nn.rhs_norm = sqrt(sqnorm(lp.h, lp.m1) + sqnorm(lp.b, lp.m2));
+  nn.obj_norm = norm2(lp.c, lp.n);
+  point_eval_t ev = evaluate_point(&lp, x, y);
+  out[0] = termination_met(&ev.res, eps, &nn);
+  out[1] = ev.res.prn;
+  out[2] = ev.res.drn;
+  out[3] = ev.res.pobj;
+  out[4] = ev.res.dobj;
+  reduced_free(&ev.red);
+  lp_free(&lp);
+  return PDLP_OK;
+}
+
 int oracle_from_triplets(int64_t rows, int64_t cols, int64_t nt, const int64_t* tr, const int64_t* tc,
                          const double* tv, int64_t* off, int64_t* col, double* val, int64_t* nnz_out) {
   csr_t m;

@@ -58,6 +58,11 @@ int oracle_from_triplets(int64_t rows, int64_t cols, int64_t nt, const int64_t* 
                          const int64_t* tc, const double* tv, int64_t* row_offsets,
                          int64_t* col_indices, double* values, int64_t* nnz_out);
 
+/* check_termination + reduced_costs at an unscaled point (solver.hpp:231-249,
+ * lp_model.hpp:192-195): out = {terminated, prn, drn, pobj_raw, dobj_raw}. */
+int oracle_check_termination(const pdlp_lp* lp, const double* x, const double* y, double eps,
+                             double* out);
+
 const char* oracle_last_error(void);
 
 #ifdef __cplusplus

@@ -498,6 +498,26 @@ int ref_from_triplets(int64_t rows, int64_t cols, int64_t nt, const int64_t* tr,
   }
 }
 
+int ref_check_termination(const pdlp_lp* lp, const double* x, const double* y, double eps,
+                          double* out) {
+  try {
+    const GeneralFormLp g = to_lp(*lp);
+    PrimalDualPoint z;
+    z.primal.assign(x, x + g.num_variables());
+    z.dual.assign(y, y + g.num_constraints());
+    const ReducedCosts rc = reduced_costs(g, z.dual);
+    const TerminationCheck c = check_termination(g, z, rc, eps, termination_norms(g));
+    out[0] = c.terminated ? 1.0 : 0.0;
+    out[1] = c.info.primal_residual_norm;
+    out[2] = c.info.dual_residual_norm;
+    out[3] = c.info.primal_objective_raw;
+    out[4] = c.info.dual_objective_raw;
+    return PDLP_OK;
+  } catch (const std::exception& e) {
+    return fail(PDLP_EINVAL, e.what());
+  }
+}
+
 // MPS loading through the reference parser (fixture generation only).
 // Two-phase: ref_mps_load parses and keeps the instance; ref_mps_sizes reports
 // {n, m1, m2, nnzG, nnzA}; ref_mps_fill copies into caller buffers.

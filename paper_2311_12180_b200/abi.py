@@ -93,6 +93,7 @@ class PdlpResultInfo(C.Structure):
         ("restarts", C.c_int64),
         ("solve_seconds", C.c_double),
         ("setup_seconds", C.c_double),
+        ("device_seconds", C.c_double),
         ("primal_objective", C.c_double),
         ("dual_objective", C.c_double),
         ("primal_objective_raw", C.c_double),

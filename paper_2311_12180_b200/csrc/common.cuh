@@ -28,8 +28,9 @@ struct InvalidArgument : std::invalid_argument {
 constexpr int kThreads = 256;        // CTA size of every tiled kernel
 constexpr int kWarps = kThreads / 32;
 constexpr int kStreamNnz = 2048;     // nnz staged per STREAM tile (8 per thread)
+constexpr int kStreamRows = 1024;    // rows per STREAM tile (each thread sums up to 4)
 constexpr int kStreamMaxRow = 32;    // rows up to this length go to STREAM tiles
-constexpr int kWarpMaxRow = 512;     // (32, 512] -> one warp per row, 8 rows per tile
+constexpr int kWarpMaxRow = 2048;    // (32, 2048] -> one warp per row, 8 rows per tile
 constexpr int kChunkNnz = 4096;      // longer rows split into chunks of this many nnz
 constexpr int kVecPad = 8;           // index/value arrays padded for 128-bit tail loads
 

@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 
@@ -69,6 +70,8 @@ Solver::Solver(const pdlp_lp& lp, const pdlp_params& params) : params_(params) {
 }
 
 Solver::~Solver() {
+  if (ev_begin_) cudaEventDestroy(ev_begin_);
+  if (ev_end_) cudaEventDestroy(ev_end_);
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
   if (graph_) cudaGraphDestroy(graph_);
   if (stream_) cudaStreamDestroy(stream_);
@@ -200,10 +203,17 @@ void Solver::setup(const pdlp_lp& lp) {
   PDLP_CUDA(cudaStreamSynchronize(s));
   K_ = DevCsr{k_rp_.get(), k_col_.get(), k_val_.get(), k_val_orig_.get(), int(m_), int(n_), nnz_};
   KT_ = DevCsr{kt_rp_.get(), kt_col_.get(), kt_val_.get(), kt_val_orig_.get(), int(n_), int(m_), nnz_};
-  k_plan_ = plan_tiles<int>(m_, rp_h.data(), parity(), kStreamMaxRow, kWarpMaxRow, kChunkNnz,
-                            kStreamNnz, kThreads);
-  kt_plan_ = plan_tiles<int>(n_, rpt_h.data(), parity(), kStreamMaxRow, kWarpMaxRow, kChunkNnz,
-                             kStreamNnz, kThreads);
+  // planner thresholds (env overrides are a tuning aid; defaults in common.cuh)
+  auto knob = [](const char* name, int def) {
+    const char* v = std::getenv(name);
+    return v ? std::atoi(v) : def;
+  };
+  const int smax = std::min(knob("PDLP_STREAM_MAX_ROW", kStreamMaxRow), kStreamNnz);
+  const int wmax = knob("PDLP_WARP_MAX_ROW", kWarpMaxRow);
+  const int cnnz = knob("PDLP_CHUNK_NNZ", kChunkNnz);
+  const int srows = std::min(knob("PDLP_STREAM_ROWS", kStreamRows), kStreamNnz);
+  k_plan_ = plan_tiles<int>(m_, rp_h.data(), parity(), smax, wmax, cnnz, kStreamNnz, srows, kThreads);
+  kt_plan_ = plan_tiles<int>(n_, rpt_h.data(), parity(), smax, wmax, cnnz, kStreamNnz, srows, kThreads);
   plan(K_, rp_h, k_plan_.tiles, k_tiles_, k_chunk_, k_ctr_);
   plan(KT_, rpt_h, kt_plan_.tiles, kt_tiles_, kt_chunk_, kt_ctr_);
   K_.chunk_slots = k_plan_.chunk_slots;
@@ -498,6 +508,11 @@ void Solver::iterate_begin(int32_t* status) {
   begun_ = true;
   state_valid_ = true;
   std::memset(&info_, 0, sizeof info_);
+  if (!ev_begin_) {
+    PDLP_CUDA(cudaEventCreate(&ev_begin_));
+    PDLP_CUDA(cudaEventCreate(&ev_end_));
+  }
+  PDLP_CUDA(cudaEventRecord(ev_begin_, stream_));
   upload_state();
   launch_zero_iterate(it_, stream_);  // z = 0, Kx = K 0 = 0, K'y = 0 (solver.hpp:764-769)
   ++launches_;
@@ -761,6 +776,13 @@ void Solver::finish(int status, int slot_x, int slot_y, int slot_lam, const KktH
   in.restarts = outer_;
   in.solve_seconds = elapsed();
   in.setup_seconds = setup_seconds_;
+  {
+    PDLP_CUDA(cudaEventRecord(ev_end_, s));
+    PDLP_CUDA(cudaEventSynchronize(ev_end_));
+    float ms = 0.f;
+    PDLP_CUDA(cudaEventElapsedTime(&ms, ev_begin_, ev_end_));
+    in.device_seconds = 1e-3 * double(ms);
+  }
   in.step_log_size = int64_t(step_log_.size());
   in.restart_log_size = int64_t(restart_log_.size());
   in.num_variables = n_;

@@ -168,6 +168,7 @@ class Solver {
   bool begun_ = false, finished_ = false, state_valid_ = false;
   int64_t launches_ = 0, evaluations_ = 0;
   double setup_seconds_ = 0.0;
+  cudaEvent_t ev_begin_ = nullptr, ev_end_ = nullptr;
   std::vector<pdlp_step_log_entry> step_log_;
   std::vector<pdlp_restart_event> restart_log_;
   pdlp_result_info info_{};

@@ -112,8 +112,7 @@ __device__ void run_tile(const Tile& t, const int* __restrict__ rp, const int* _
       }
     }
     __syncthreads();
-    const int r = t.row0 + tid;
-    if (r < t.row1) {
+    for (int r = t.row0 + tid; r < t.row1; r += kThreads) {
       const int a = rp[r] - t.k0, b = rp[r + 1] - t.k0;
       double acc[Epi::NA];
       zero_acc<Epi>(acc);
@@ -211,14 +210,23 @@ __device__ __forceinline__ bool grid_last_block(unsigned* counter, unsigned tota
 template <int NS, int NM>
 __device__ __forceinline__ void sum_partials(const double* partials, int count, double (&out)[NS + NM]) {
   constexpr int K = NS + NM;
+  constexpr int B = K <= 4 ? 8 : 2;  // loads in flight per thread
   __shared__ double sred[kWarps * K];
 #pragma unroll
   for (int i = 0; i < K; ++i) out[i] = i < NS ? 0.0 : -INFINITY;
-  for (int j = threadIdx.x; j < count; j += kThreads) {
+  for (int j0 = threadIdx.x; j0 < count; j0 += kThreads * B) {
+    double v[B][K];
 #pragma unroll
-    for (int i = 0; i < K; ++i) {
-      const double v = __ldcg(partials + size_t(j) * K + i);
-      out[i] = i < NS ? out[i] + v : fmax(out[i], v);
+    for (int b = 0; b < B; ++b) {
+      const int j = j0 + b * kThreads;
+#pragma unroll
+      for (int i = 0; i < K; ++i)
+        v[b][i] = j < count ? __ldcg(partials + size_t(j) * K + i) : (i < NS ? 0.0 : -INFINITY);
+    }
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+#pragma unroll
+      for (int i = 0; i < K; ++i) out[i] = i < NS ? out[i] + v[b][i] : fmax(out[i], v[b][i]);
     }
   }
   block_reduce<NS, NM>(out, sred);

@@ -7,7 +7,7 @@ namespace pdlp {
 
 template <class Off>
 TilePlan plan_tiles(int64_t rows, const Off* rp, bool parity, int stream_max_row,
-                    int warp_max_row, int chunk_nnz, int stream_nnz, int threads) {
+                    int warp_max_row, int chunk_nnz, int stream_nnz, int stream_rows, int threads) {
   TilePlan plan;
   int64_t r = 0;
   auto len = [&](int64_t i) { return int64_t(rp[i + 1] - rp[i]); };
@@ -15,7 +15,7 @@ TilePlan plan_tiles(int64_t rows, const Off* rp, bool parity, int stream_max_row
     const int64_t l = len(r);
     if (l <= stream_max_row) {
       const int64_t r0 = r, k0 = rp[r];
-      while (r < rows && r - r0 < threads && len(r) <= stream_max_row &&
+      while (r < rows && r - r0 < stream_rows && len(r) <= stream_max_row &&
              int64_t(rp[r + 1]) - k0 <= stream_nnz)
         ++r;
       plan.tiles.push_back({kTileStream, int32_t(r0), int32_t(r), int32_t(k0), int32_t(rp[r]), 0, 1, 0});
@@ -50,7 +50,7 @@ TilePlan plan_tiles(int64_t rows, const Off* rp, bool parity, int stream_max_row
   return plan;
 }
 
-template TilePlan plan_tiles<int>(int64_t, const int*, bool, int, int, int, int, int);
-template TilePlan plan_tiles<int64_t>(int64_t, const int64_t*, bool, int, int, int, int, int);
+template TilePlan plan_tiles<int>(int64_t, const int*, bool, int, int, int, int, int, int);
+template TilePlan plan_tiles<int64_t>(int64_t, const int64_t*, bool, int, int, int, int, int, int);
 
 }  // namespace pdlp

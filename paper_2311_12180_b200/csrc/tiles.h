@@ -45,6 +45,6 @@ struct TilePlan {
 // `parity` disables WARP tiles and row splitting.
 template <class Off>
 TilePlan plan_tiles(int64_t rows, const Off* rp, bool parity, int stream_max_row,
-                    int warp_max_row, int chunk_nnz, int stream_nnz, int threads);
+                    int warp_max_row, int chunk_nnz, int stream_nnz, int stream_rows, int threads);
 
 }  // namespace pdlp
