@@ -77,6 +77,19 @@ enum {
   PDLP_MODE_PARITY = 1
 };
 
+/* ---- iteration engines (B200 extension) ----------------------------- */
+enum {
+  /* GRAPH (STREAM if use_cuda_graph == 0) */
+  PDLP_ENGINE_AUTO = 0,
+  /* one cooperative persistent kernel per evaluation window: TMA-fed tile
+   * pipeline, grid barriers, on-device step decisions (fast mode only) */
+  PDLP_ENGINE_PERSISTENT = 1,
+  /* CUDA graph: WHILE(conditional node) { dual kernel; primal kernel } */
+  PDLP_ENGINE_GRAPH = 2,
+  /* plain stream launches of the per-trial kernels */
+  PDLP_ENGINE_STREAM = 3
+};
+
 /* CSR of one constraint block; mirrors CsrMatrix (sparse_matrix.hpp:35-55).
  * Invariants expected (as produced by CsrMatrix::from_triplets):
  * row_offsets[0]==0, row_offsets[num_rows]==nnz, nondecreasing; column indices
@@ -132,7 +145,8 @@ typedef struct {
   int32_t mode;                /* PDLP_MODE_FAST */
   int32_t use_cuda_graph;      /* 1: replay each evaluation window as a CUDA graph */
   int32_t l2_persist;          /* 1: pin the gathered iterate in L2 (access-policy window) */
-  int32_t reserved[7];
+  int32_t engine;              /* PDLP_ENGINE_*: how a window of iterations is driven */
+  int32_t reserved[6];
 } pdlp_params;
 
 /* ConvergenceInfo (solver.hpp:165-177) plus SolveResult scalars (:618-630). */
@@ -144,6 +158,7 @@ typedef struct {
   double solve_seconds;  /* loop time, excludes setup like the reference (:636-646,760) */
   double setup_seconds;  /* upload + K^T build + preconditioning (B200 extension) */
   double device_seconds; /* solve loop timed with CUDA events on the solver's stream */
+  double window_seconds; /* time inside the iteration kernels (windows), CUDA events */
   double primal_objective;
   double dual_objective;
   double primal_objective_raw;

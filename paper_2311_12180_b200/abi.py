@@ -25,6 +25,7 @@ RESTART_NAMES = ["none", "sufficient_decay", "necessary_decay_no_progress", "lon
 
 OP_K_SCALED, OP_KT_SCALED, OP_K_ORIGINAL, OP_KT_ORIGINAL = 0, 1, 2, 3
 MODE_FAST, MODE_PARITY = 0, 1
+ENGINE_AUTO, ENGINE_PERSISTENT, ENGINE_GRAPH, ENGINE_STREAM = 0, 1, 2, 3
 
 _dp = C.POINTER(C.c_double)
 _i64p = C.POINTER(C.c_int64)
@@ -81,7 +82,8 @@ class PdlpParams(C.Structure):
         ("mode", C.c_int32),
         ("use_cuda_graph", C.c_int32),
         ("l2_persist", C.c_int32),
-        ("reserved", C.c_int32 * 7),
+        ("engine", C.c_int32),
+        ("reserved", C.c_int32 * 6),
     ]
 
 
@@ -94,6 +96,7 @@ class PdlpResultInfo(C.Structure):
         ("solve_seconds", C.c_double),
         ("setup_seconds", C.c_double),
         ("device_seconds", C.c_double),
+        ("window_seconds", C.c_double),
         ("primal_objective", C.c_double),
         ("dual_objective", C.c_double),
         ("primal_objective_raw", C.c_double),

@@ -77,6 +77,7 @@ void pdlp_default_params(pdlp_params* p) {
   p->mode = PDLP_MODE_FAST;
   p->use_cuda_graph = 1;
   p->l2_persist = 1;
+  p->engine = PDLP_ENGINE_AUTO;
 }
 
 int pdlp_create(const pdlp_lp* lp, const pdlp_params* params, pdlp_handle** out) {

@@ -27,12 +27,25 @@ struct InvalidArgument : std::invalid_argument {
 
 constexpr int kThreads = 256;        // CTA size of every tiled kernel
 constexpr int kWarps = kThreads / 32;
-constexpr int kStreamNnz = 2048;     // nnz staged per STREAM tile (8 per thread)
-constexpr int kStreamRows = 1024;    // rows per STREAM tile (each thread sums up to 4)
 constexpr int kStreamMaxRow = 32;    // rows up to this length go to STREAM tiles
-constexpr int kWarpMaxRow = 2048;    // (32, 2048] -> one warp per row, 8 rows per tile
-constexpr int kChunkNnz = 4096;      // longer rows split into chunks of this many nnz
+constexpr int kWarpMaxRow = 4096;    // (32, 4096] -> a lane group per row (tiles.h)
 constexpr int kVecPad = 8;           // index/value arrays padded for 128-bit tail loads
+
+// Tile geometry per kernel family (tiles.h). The iteration kernels take fat
+// tiles (16 nnz per thread) so C2-sized operators run in about one wave; the
+// persistent window kernel stages whole tiles in shared memory; the evaluation
+// kernels gather 4 values per nonzero and keep their staging small.
+struct TileGeom {
+  int stream_nnz;  // nnz per STREAM tile (staged products in shared memory)
+  int stream_rows; // rows per STREAM tile = rows_per_thread * kThreads
+  int lane_nnz;    // target nnz per lane in WARP tiles
+  int chunk_nnz;   // nnz per CHUNK tile of a split row
+};
+constexpr TileGeom kIterGeom{4096, 2048, 16, 4096};
+constexpr TileGeom kWinGeom{2048, 1024, 8, 2048};
+constexpr TileGeom kEvalGeom{1024, 1024, 8, 2048};
+constexpr int kStreamNnz = 4096;     // largest STREAM tile of any geometry
+constexpr int kStreamRows = 2048;
 
 // ---------------------------------------------------------------------------
 // IEEE helpers with the reference's semantics (libstdc++ std::min/std::max are
@@ -55,6 +68,18 @@ __device__ __forceinline__ double2 ld_stream_d2(const double* p) {
                : "=d"(r.x), "=d"(r.y)
                : "l"(p));
   return r;
+}
+
+// Programmatic dependent launch (PDL): a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start while its
+// predecessor drains; everything before griddep_wait() must only touch data the
+// predecessor does not write (static matrix, tile plan).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
 }
 
 // Fixed-order warp sum (xor butterfly): identical result on every replay.

@@ -39,6 +39,8 @@ struct DevState {
   double eta_acc, eta_bar, eta_next, mov, inter;  // last accepted step
   unsigned ctr_dual;
   unsigned ctr_eval;
+  int32_t window_cont;  // set by the window kernel's decision: run another trial
+  int32_t pad2;
 };
 
 // Results of one evaluation block (evaluate_candidates + the infeasibility
@@ -86,9 +88,13 @@ struct DevIter {
   const double* q;   // scaled rhs (h; b)
   int n, m, m1;
   int p_grid;        // CTAs of the primal kernel
+  int nonneg;        // every scaled bound is l = +0, u = +inf: clamp is max(v, 0)
   int avg_blocks;    // trailing CTAs of the primal kernel that update avg_y
   double* d_part;    // [K tiles * 3]
-  double* p_part;    // [p_grid * 2]
+  double* p_part;    // [2][p_grid * 2], ping-pong by trial parity
+  double* px_total;  // unused (kept for layout stability)
+  DevState* snap;    // state the current trial's dual kernel ran on (fast mode)
+  int d_tiles;       // CTAs of the dual kernel (partials the decision sums)
   double* seq_dy2;   // parity-mode per-row terms (m)
   double* seq_inter; // (m)
   double* seq_dx2;   // (n)

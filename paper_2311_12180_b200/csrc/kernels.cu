@@ -18,76 +18,23 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <utility>
+
 #include "../../include/pdlp_b200.h"
 #include "kernels.cuh"
+#include "epilogues.cuh"
 #include "spmv_engine.cuh"
 
 namespace pdlp {
 
 namespace {
-
-__device__ __forceinline__ double clamp_box(double v, double l, double u) {
-  return smin(smax(v, l), u);  // std::min(std::max(x, l), u), vector_ops.hpp:56
-}
-
-// reduced_costs_from_slack (lp_model.hpp:155-174), one component.
-__device__ __forceinline__ double reduced_cost(double v, double l, double u) {
-  const bool lf = l > -INFINITY, uf = u < INFINITY;
-  if (lf && uf) return v;
-  if (lf) return smax(v, 0.0);
-  if (uf) return smin(v, 0.0);
-  return 0.0;
-}
-
-// l'lambda+ - u'lambda- contribution of one component (lp_model.hpp:248-251).
-__device__ __forceinline__ double lambda_term(double lam, double l, double u) {
-  if (lam > 0.0) return l * lam;
-  if (lam < 0.0) return -(u * -lam);
-  return 0.0;
-}
-
 int ceil_div(int64_t a, int64_t b) { return int((a + b - 1) / b); }
-
 }  // namespace
 
 // ===========================================================================
 // Iteration: dual kernel
 // ===========================================================================
 
-template <bool kSeq>
-struct DualEpi {
-  static constexpr int NP = 1, NA = 1, NR = 3;
-  static constexpr bool kNeedCol = false;
-  const double* __restrict__ xg;
-  const double* __restrict__ y;
-  const double* __restrict__ kx;
-  const double* __restrict__ q;
-  double* __restrict__ yt;
-  double* __restrict__ kxt;
-  double* __restrict__ seq_dy2;
-  double* __restrict__ seq_inter;
-  double sigma;
-  int m1;
-  __device__ __forceinline__ void gather(int c, double (&g)[1]) const { g[0] = __ldg(xg + c); }
-  __device__ __forceinline__ void add(double (&a)[1], const double (&p)[1], int) const { a[0] += p[0]; }
-  __device__ __forceinline__ void row_done(int r, const double (&a)[1], double (&red)[3]) const {
-    const double kxn = a[0];
-    const double kxo = kx[r], yo = y[r];
-    double yn = yo + sigma * (q[r] - 2.0 * kxn + kxo);  // solver.hpp:412-413
-    if (r < m1 && yn < 0.0) yn = 0.0;                    // project_dual_in_place
-    yt[r] = yn;
-    kxt[r] = kxn;
-    const double d = yn - yo;
-    const double dd = d * d, di = d * (kxn - kxo);
-    if (kSeq) {
-      seq_dy2[r] = dd;
-      seq_inter[r] = di;
-    }
-    red[0] += dd;
-    red[1] += di;
-    red[2] += isfinite(yn) ? 0.0 : 1.0;
-  }
-};
 
 // Sequential (reference-order) sums used by the parity mode's reductions.
 __device__ double seq_sum(const double* v, int n) {
@@ -104,15 +51,128 @@ __device__ double seq_sum_sq(const double* v, int n) {
   return s;
 }
 
+// Outcome of the step decision (adaptive_step_cached, solver.hpp:436-466).
+struct Decision {
+  int mode;  // kPAccept / kPRetry / kPNone
+  int cont;  // run another trial in this window
+  double eta;  // step size of the next trial
+  double ratio;
+  int first;
+  int ix_cur, ix_trial, iy_cur, ikty_cur;
+  int64_t trials;  // trials_total after this decision
+};
+
+// The decision from the reduced trial terms, on the pre-decision state `s`.
+// `st` (may be null) receives the new state; `log` the accepted step.
+__device__ Decision step_decision(const DevState& s, const DevIter& it, double dy2, double inter,
+                                  double dx2, bool finite, DevState* st) {
+  Decision d;
+  const double omega = s.omega, eta = s.eta;
+  d.cont = 0;
+  d.mode = kPNone;
+  d.eta = eta;
+  d.ratio = s.avg_ratio;
+  d.first = s.avg_first;
+  d.ix_cur = s.ix_cur, d.ix_trial = s.ix_trial, d.iy_cur = s.iy_cur, d.ikty_cur = s.ikty_cur;
+  d.trials = s.trials_total + 1;
+  int trials_in_step = s.trials_in_step + 1;
+  if (st) {
+    st->trials_total = d.trials;
+    st->trials_in_step = trials_in_step;
+  }
+  if (!finite) {
+    if (st) {
+      st->failure = 1;
+      st->p_mode = kPNone;
+    }
+    return d;
+  }
+  const double movement = omega * dx2 + dy2 / omega;  // solver.hpp:436
+  const double ia = fabs(inter);
+  const double eta_bar = ia > 0.0 ? movement / (2.0 * ia) : INFINITY;
+  const int64_t ti = s.total - s.table_base;
+  const double eta_next = smin(it.red_tab[ti] * eta_bar, it.gro_tab[ti] * eta);
+  d.eta = eta_next;
+  if (eta <= eta_bar) {  // accept
+    const double w = s.wsum + eta;  // WeightedAverage::add
+    d.first = (w == eta) ? 1 : 0;
+    d.ratio = eta / w;
+    d.mode = kPAccept;
+    // rotate: prev <- cur <- trial <- old prev
+    d.ix_cur = s.ix_trial, d.ix_trial = s.ix_prev;
+    d.iy_cur = s.iy_trial;
+    d.ikty_cur = 1 - s.ikty_cur;
+    d.cont = s.window_accepts + 1 < s.window_target;
+    if (st) {
+      if (s.record_log) {
+        pdlp_step_log_entry* log = reinterpret_cast<pdlp_step_log_entry*>(it.step_log);
+        pdlp_step_log_entry e;
+        e.step_counter = s.total + 1;
+        e.omega = omega;
+        e.eta_accepted = eta;
+        e.eta_bar = eta_bar;
+        e.eta_next = eta_next;
+        e.movement_sq = movement;
+        e.interaction = inter;
+        log[s.window_accepts] = e;
+      }
+      st->eta_acc = eta;
+      st->eta_bar = eta_bar;
+      st->eta_next = eta_next;
+      st->mov = movement;
+      st->inter = inter;
+      st->total = s.total + 1;
+      st->inner = s.inner + 1;
+      st->window_accepts = s.window_accepts + 1;
+      st->wsum = w;
+      st->avg_first = d.first;
+      st->avg_ratio = d.ratio;
+      st->ix_prev = s.ix_cur;
+      st->ix_cur = d.ix_cur;
+      st->ix_trial = d.ix_trial;
+      st->iy_prev = s.iy_cur;
+      st->iy_cur = d.iy_cur;
+      st->iy_trial = s.iy_prev;
+      st->ikx_cur = 1 - s.ikx_cur;
+      st->ikty_cur = d.ikty_cur;
+      st->eta = eta_next;
+      st->trials_in_step = 0;
+      st->accepted = 1;
+      st->p_mode = kPAccept;
+    }
+  } else {  // reject: shrink the step
+    const bool bad = !(eta_next > 0.0) || !isfinite(eta_next) || trials_in_step >= 80;
+    d.mode = bad ? kPNone : kPRetry;
+    d.cont = bad ? 0 : 1;
+    if (st) {
+      st->eta = eta_next;
+      st->accepted = 0;
+      st->failure = bad ? 1 : 0;
+      st->p_mode = d.mode;
+    }
+  }
+  return d;
+}
+
+// Dual side of a trial: K x' fused with the projected dual update and the dy^2 /
+// interaction partials. In fast mode the step decision is taken at the head of
+// the primal kernel (every primal CTA recomputes it from the same partials in
+// the same order), so this kernel has no serial tail; CTA 0 snapshots the state
+// the decision will start from. Parity mode keeps the decision here (last CTA),
+// where the reference-order sequential sums run.
 template <bool kSeq>
-__global__ void __launch_bounds__(kThreads) dual_kernel(DevCsr K, DevIter it,
-                                                        cudaGraphConditionalHandle cond,
-                                                        int use_cond) {
+__global__ void __launch_bounds__(kThreads, 4) dual_kernel(DevCsr K, DevIter it,
+                                                           cudaGraphConditionalHandle cond,
+                                                           int use_cond) {
   extern __shared__ __align__(16) unsigned char smem[];
+  const Tile t = K.tiles[blockIdx.x];
+  prefetch_tile(t, K.rp, K.col, K.val);
+  griddep_wait();  // x' and the state come from the previous primal kernel
   DevState* st = it.st;
-  // A failed or completed window parks the remaining (fallback-mode) launches.
+  if (!kSeq && blockIdx.x == 0 && threadIdx.x == 0) *it.snap = *st;
+  // A failed or completed window parks the remaining (stream-engine) launches.
   if (st->failure || st->window_accepts >= st->window_target) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) st->p_mode = kPNone;
+    if (kSeq && blockIdx.x == 0 && threadIdx.x == 0) st->p_mode = kPNone;
     return;
   }
   DualEpi<kSeq> epi;
@@ -127,202 +187,140 @@ __global__ void __launch_bounds__(kThreads) dual_kernel(DevCsr K, DevIter it,
   epi.sigma = st->eta * st->omega;  // sigma = eta * omega, solver.hpp:402
   epi.m1 = it.m1;
   double red[3] = {0.0, 0.0, 0.0};
-  const Tile t = K.tiles[blockIdx.x];
   run_tile<DualEpi<kSeq>, kSeq>(t, K.rp, K.col, K.val, epi, red, K.chunk_part, K.chunk_ctr, smem);
+  // the primal kernel's CTAs may start their prologue once every dual CTA is
+  // past its tile (triggering earlier would let them take slots from our waves)
+  griddep_launch_dependents();
   store_partial<3, 0>(red, it.d_part, blockIdx.x);
-  if (!grid_last_block(&st->ctr_dual, gridDim.x)) return;
+  if (!kSeq) return;
 
-  // ---- last CTA: reductions and the step decision ----
+  // ---- parity mode: the decision in the last CTA, sums in reference order ----
+  if (!grid_last_block(&st->ctr_dual, gridDim.x)) return;
   double dpart[3], ppart[2];
   sum_partials<3, 0>(it.d_part, gridDim.x, dpart);
-  sum_partials<2, 0>(it.p_part, it.p_grid, ppart);
+  sum_partials<2, 0>(it.p_part + size_t(st->trials_total & 1) * it.p_grid * 2, it.p_grid, ppart);
   if (threadIdx.x != 0) return;
-  double dy2 = dpart[0], inter = dpart[1], dx2 = ppart[0];
-  if (kSeq) {  // the reference's sequential index order (solver.hpp:422-435)
-    dx2 = seq_sum(it.seq_dx2, it.n);
-    double a = 0.0, b = 0.0;
-    for (int i = 0; i < it.m; ++i) {
-      a += __ldcg(it.seq_dy2 + i);
-      b += __ldcg(it.seq_inter + i);
-    }
-    dy2 = a;
-    inter = b;
+  const double dx2 = seq_sum(it.seq_dx2, it.n);  // solver.hpp:422-435
+  double dy2 = 0.0, inter = 0.0;
+  for (int i = 0; i < it.m; ++i) {
+    dy2 += __ldcg(it.seq_dy2 + i);
+    inter += __ldcg(it.seq_inter + i);
   }
-  const bool finite = dpart[2] == 0.0 && ppart[1] == 0.0;
-  const double omega = st->omega, eta = st->eta;
-  int cont = 0;
-  st->trials_total += 1;
-  st->trials_in_step += 1;
-  if (!finite) {
-    st->failure = 1;
-    st->p_mode = kPNone;
-  } else {
-    const double movement = omega * dx2 + dy2 / omega;  // solver.hpp:436
-    const double ia = fabs(inter);
-    const double eta_bar = ia > 0.0 ? movement / (2.0 * ia) : INFINITY;
-    const int64_t ti = st->total - st->table_base;
-    const double eta_next = smin(it.red_tab[ti] * eta_bar, it.gro_tab[ti] * eta);
-    if (eta <= eta_bar) {
-      if (st->record_log) {
-        pdlp_step_log_entry* log = reinterpret_cast<pdlp_step_log_entry*>(it.step_log);
-        pdlp_step_log_entry e;
-        e.step_counter = st->total + 1;
-        e.omega = omega;
-        e.eta_accepted = eta;
-        e.eta_bar = eta_bar;
-        e.eta_next = eta_next;
-        e.movement_sq = movement;
-        e.interaction = inter;
-        log[st->window_accepts] = e;
-      }
-      st->eta_acc = eta;
-      st->eta_bar = eta_bar;
-      st->eta_next = eta_next;
-      st->mov = movement;
-      st->inter = inter;
-      st->total += 1;
-      st->inner += 1;
-      st->window_accepts += 1;
-      const double w = st->wsum + eta;  // WeightedAverage::add
-      st->wsum = w;
-      st->avg_first = (w == eta) ? 1 : 0;
-      st->avg_ratio = eta / w;
-      // rotate: prev <- cur <- trial <- old prev
-      int t0 = st->ix_prev;
-      st->ix_prev = st->ix_cur;
-      st->ix_cur = st->ix_trial;
-      st->ix_trial = t0;
-      t0 = st->iy_prev;
-      st->iy_prev = st->iy_cur;
-      st->iy_cur = st->iy_trial;
-      st->iy_trial = t0;
-      st->ikx_cur = 1 - st->ikx_cur;
-      st->ikty_cur = 1 - st->ikty_cur;
-      st->eta = eta_next;
-      st->trials_in_step = 0;
-      st->accepted = 1;
-      st->p_mode = kPAccept;
-      cont = st->window_accepts < st->window_target;
-    } else {
-      st->eta = eta_next;
-      st->accepted = 0;
-      if (!(eta_next > 0.0) || !isfinite(eta_next) || st->trials_in_step >= 80) {
-        st->failure = 1;
-        st->p_mode = kPNone;
-      } else {
-        st->p_mode = kPRetry;
-        cont = 1;
-      }
-    }
-  }
+  const DevState pre = *st;
+  const Decision d = step_decision(pre, it, dy2, inter, dx2, dpart[2] == 0.0 && ppart[1] == 0.0, st);
   __threadfence();
-  if (use_cond) cudaGraphSetConditional(cond, cont ? 1u : 0u);
+  if (use_cond) cudaGraphSetConditional(cond, d.cont ? 1u : 0u);
 }
 
 // ===========================================================================
 // Iteration: primal kernel
 // ===========================================================================
 
-template <bool kSeq>
-struct PrimalEpi {
-  static constexpr int NP = 1, NA = 1, NR = 2;
-  static constexpr bool kNeedCol = false;
-  const double* __restrict__ yg;
-  const double* __restrict__ xc;
-  const double* __restrict__ c;
-  const double* __restrict__ l;
-  const double* __restrict__ u;
-  double* __restrict__ kty_out;
-  double* __restrict__ xt;
-  double* __restrict__ avg_x;
-  double* __restrict__ seq_dx2;
-  double tau;
-  double ratio;
-  int do_avg;
-  int avg_first;
-  __device__ __forceinline__ void gather(int r, double (&g)[1]) const { g[0] = __ldg(yg + r); }
-  __device__ __forceinline__ void add(double (&a)[1], const double (&p)[1], int) const { a[0] += p[0]; }
-  __device__ __forceinline__ void row_done(int j, const double (&a)[1], double (&red)[2]) const {
-    const double s = a[0];
-    kty_out[j] = s;
-    const double xa = xc[j];
-    if (do_avg) avg_x[j] = avg_first ? xa : avg_x[j] + ratio * (xa - avg_x[j]);
-    const double xn = clamp_box(xa - tau * (c[j] - s), l[j], u[j]);  // solver.hpp:404-408
-    xt[j] = xn;
-    const double d = xn - xa;
-    const double dd = d * d;
-    if (kSeq) seq_dx2[j] = dd;
-    red[0] += dd;
-    red[1] += isfinite(xn) ? 0.0 : 1.0;
-  }
-};
-
-template <bool kSeq>
-__global__ void __launch_bounds__(kThreads) primal_kernel(DevCsr KT, DevIter it, int mode_override) {
+// Primal side of a trial. mode_override >= 0 forces a branch (first trial of a
+// solve: retry; after a restart: restart). Otherwise the fast mode takes the
+// step decision first (all CTAs, CTA 0 commits it), parity mode reads it.
+template <bool kSeq, bool kNonneg>
+__global__ void __launch_bounds__(kThreads, 4) primal_kernel(DevCsr KT, DevIter it, int mode_override,
+                                                             cudaGraphConditionalHandle cond,
+                                                             int use_cond) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const DevState* st = it.st;
-  const int mode = mode_override >= 0 ? mode_override : st->p_mode;
-  if (mode == kPNone) return;  // keep the partials of the last real trial
-  double red[2] = {0.0, 0.0};
-  const double tau = st->eta / st->omega;  // tau = eta / omega, solver.hpp:401
+  __shared__ Decision sd;
+  if (int(blockIdx.x) < KT.ntiles) {
+    const Tile tp = KT.tiles[blockIdx.x];
+    prefetch_tile(tp, KT.rp, KT.col, KT.val);
+  }
+  griddep_wait();  // y' and the dual partials come from the dual kernel
+  DevState* st = it.st;
   const int bid = blockIdx.x;
-  if (mode == kPAccept || mode == kPRestart) {
-    const bool acc = mode == kPAccept;
+  Decision d;
+  if (mode_override >= 0 || kSeq) {
+    const DevState& s = *st;
+    d.mode = mode_override >= 0 ? mode_override : s.p_mode;
+    d.eta = s.eta;
+    d.ratio = s.avg_ratio;
+    d.first = s.avg_first;
+    d.ix_cur = s.ix_cur, d.ix_trial = s.ix_trial, d.iy_cur = s.iy_cur, d.ikty_cur = s.ikty_cur;
+    d.trials = s.trials_total;
+  } else {
+    const DevState& s = *it.snap;  // the state the dual kernel of this trial ran on
+    if (s.failure || s.window_accepts >= s.window_target) return;
+    double dp[3], pp[2];
+    sum_partials<3, 0>(it.d_part, it.d_tiles, dp);
+    sum_partials<2, 0>(it.p_part + size_t(s.trials_total & 1) * it.p_grid * 2, it.p_grid, pp);
+    if (threadIdx.x == 0) {
+      const bool commit = bid == 0;
+      sd = step_decision(s, it, dp[0], dp[1], pp[0], dp[2] == 0.0 && pp[1] == 0.0,
+                         commit ? st : nullptr);
+      if (commit) {
+        __threadfence();
+        if (use_cond) cudaGraphSetConditional(cond, sd.cont ? 1u : 0u);
+      }
+    }
+    __syncthreads();
+    d = sd;
+  }
+  if (d.mode == kPNone) return;  // keep the partials of the last real trial
+  double red[2] = {0.0, 0.0};
+  const double tau = d.eta / st->omega;  // tau = eta / omega, solver.hpp:401
+  if (d.mode == kPAccept || d.mode == kPRestart) {
+    const bool acc = d.mode == kPAccept;
     if (bid < KT.ntiles) {
-      PrimalEpi<kSeq> epi;
-      epi.yg = it.y[st->iy_cur];
-      epi.xc = it.x[st->ix_cur];
+      PrimalEpi<kSeq, kNonneg> epi;
+      epi.yg = it.y[d.iy_cur];
+      epi.xc = it.x[d.ix_cur];
       epi.c = it.c;
       epi.l = it.l;
       epi.u = it.u;
-      epi.kty_out = it.kty[st->ikty_cur];
-      epi.xt = it.x[st->ix_trial];
+      epi.kty_out = it.kty[d.ikty_cur];
+      epi.xt = it.x[d.ix_trial];
       epi.avg_x = it.avg_x;
       epi.seq_dx2 = it.seq_dx2;
       epi.tau = tau;
-      epi.ratio = st->avg_ratio;
+      epi.ratio = d.ratio;
       epi.do_avg = acc;
-      epi.avg_first = st->avg_first;
+      epi.avg_first = d.first;
       const Tile t = KT.tiles[bid];
-      run_tile<PrimalEpi<kSeq>, kSeq>(t, KT.rp, KT.col, KT.val, epi, red, KT.chunk_part,
-                                      KT.chunk_ctr, smem);
+      run_tile<PrimalEpi<kSeq, kNonneg>, kSeq>(t, KT.rp, KT.col, KT.val, epi, red, KT.chunk_part,
+                                               KT.chunk_ctr, smem);
     } else if (acc) {
       // avg_y .add (solver.hpp:839) on this CTA's slice of the dual vector
       const int nb = it.avg_blocks, b = bid - KT.ntiles;
       const int per = (it.m + nb - 1) / nb;
       const int i0 = b * per, i1 = min(it.m, i0 + per);
-      const double* yc = it.y[st->iy_cur];
-      const double ratio = st->avg_ratio;
-      const int first = st->avg_first;
+      const double* yc = it.y[d.iy_cur];
       for (int i = i0 + threadIdx.x; i < i1; i += kThreads)
-        it.avg_y[i] = first ? yc[i] : it.avg_y[i] + ratio * (yc[i] - it.avg_y[i]);
+        it.avg_y[i] = d.first ? yc[i] : it.avg_y[i] + d.ratio * (yc[i] - it.avg_y[i]);
     }
-  } else if (mode == kPRetry) {
+  } else if (d.mode == kPRetry) {
     const int per = (it.n + gridDim.x - 1) / gridDim.x;
     const int j0 = bid * per, j1 = min(it.n, j0 + per);
-    const double* xc = it.x[st->ix_cur];
-    const double* kty = it.kty[st->ikty_cur];
-    double* xt = it.x[st->ix_trial];
+    const double* xc = it.x[d.ix_cur];
+    const double* kty = it.kty[d.ikty_cur];
+    double* xt = it.x[d.ix_trial];
     for (int j = j0 + threadIdx.x; j < j1; j += kThreads) {
       const double xa = xc[j];
-      const double xn = clamp_box(xa - tau * (it.c[j] - kty[j]), it.l[j], it.u[j]);
+      const double v = xa - tau * (it.c[j] - kty[j]);
+      const double xn = kNonneg ? smax(v, 0.0) : clamp_box(v, it.l[j], it.u[j]);
       xt[j] = xn;
-      const double d = xn - xa;
-      const double dd = d * d;
+      const double dd = (xn - xa) * (xn - xa);
       if (kSeq) it.seq_dx2[j] = dd;
       red[0] += dd;
       red[1] += isfinite(xn) ? 0.0 : 1.0;
     }
   }
-  store_partial<2, 0>(red, it.p_part, bid);
+  griddep_launch_dependents();
+  // ping-pong by trial parity: the next decision reads these while this launch's
+  // late CTAs may still be reading the previous ones
+  store_partial<2, 0>(red, it.p_part + size_t(d.trials & 1) * it.p_grid * 2, bid);
 }
 
 // ===========================================================================
 // Plain SpMV (kernel parity API and restart products)
 // ===========================================================================
 
-struct MatvecEpi {
+struct MatvecEpi : EpiBase<MatvecEpi> {
   static constexpr int NP = 1, NA = 1, NR = 1;
+  static constexpr TileGeom kGeom = kIterGeom;
   static constexpr bool kNeedCol = false;
   const double* __restrict__ x;
   double* __restrict__ out;
@@ -337,7 +335,9 @@ template <bool kSeq>
 __global__ void __launch_bounds__(kThreads) spmv_kernel(DevCsr A, const double* val,
                                                         const double* x, double* out) {
   extern __shared__ __align__(16) unsigned char smem[];
-  MatvecEpi epi{x, out};
+  MatvecEpi epi;
+  epi.x = x;
+  epi.out = out;
   double red[1] = {0.0};
   const Tile t = A.tiles[blockIdx.x];
   run_tile<MatvecEpi, kSeq>(t, A.rp, A.col, val, epi, red, A.chunk_part, A.chunk_ctr, smem);
@@ -456,8 +456,9 @@ __device__ __forceinline__ void load4(const double* p, double (&g)[4]) {
 // Reductions: [0..5] KKT slots (viol^2, eq^2, q'y) x2, [6..11] ray slots
 // (|Ax|^2, |y|^2, q'y) x2; maxima [12..13]: max_i(-Gx_i) per ray.
 template <bool kSeq>
-struct Ev1Epi {
+struct Ev1Epi : EpiBase<Ev1Epi<kSeq>> {
   static constexpr int NP = 4, NA = 4, NR = 14;
+  static constexpr TileGeom kGeom = kEvalGeom;
   static constexpr bool kNeedCol = false;
   const double* __restrict__ X4;
   const double* __restrict__ Y4;
@@ -513,8 +514,9 @@ struct Ev1Epi {
 // c'x) x2 = [6..13]; maxima [14..17]: (max -x over finite l, max x over finite u)
 // per ray.
 template <bool kSeq>
-struct Ev2Epi {
+struct Ev2Epi : EpiBase<Ev2Epi<kSeq>> {
   static constexpr int NP = 4, NA = 8, NR = 18;
+  static constexpr TileGeom kGeom = kEvalGeom;
   static constexpr bool kNeedCol = true;
   const double* __restrict__ Y4;
   const double* __restrict__ X4;
@@ -571,7 +573,8 @@ struct Ev2Epi {
 template <bool kSeq>
 __global__ void __launch_bounds__(kThreads) eval_rows_kernel(DevCsr K, DevEval ev, int m, int m1) {
   extern __shared__ __align__(16) unsigned char smem[];
-  Ev1Epi<kSeq> epi{ev.X4, ev.Y4, ev.q, ev.seq_r, m, m1};
+  Ev1Epi<kSeq> epi;
+  epi.X4 = ev.X4, epi.Y4 = ev.Y4, epi.q = ev.q, epi.seq_r = ev.seq_r, epi.m = m, epi.m1 = m1;
   double red[14];
 #pragma unroll
   for (int i = 0; i < 14; ++i) red[i] = i < 12 ? 0.0 : -INFINITY;
@@ -583,7 +586,9 @@ __global__ void __launch_bounds__(kThreads) eval_rows_kernel(DevCsr K, DevEval e
 template <bool kSeq>
 __global__ void __launch_bounds__(kThreads) eval_cols_kernel(DevCsr KT, DevEval ev, int n, int m1) {
   extern __shared__ __align__(16) unsigned char smem[];
-  Ev2Epi<kSeq> epi{ev.Y4, ev.X4, ev.c, ev.l, ev.u, ev.lam, ev.seq_d, n, m1};
+  Ev2Epi<kSeq> epi;
+  epi.Y4 = ev.Y4, epi.X4 = ev.X4, epi.c = ev.c, epi.l = ev.l, epi.u = ev.u, epi.lam = ev.lam;
+  epi.seq_d = ev.seq_d, epi.n = n, epi.m1 = m1;
   double red[18];
 #pragma unroll
   for (int i = 0; i < 18; ++i) red[i] = i < 14 ? 0.0 : -INFINITY;
@@ -1019,25 +1024,50 @@ void launch_spmv(const DevCsr& a, bool orig_vals, const double* x, double* out, 
   PDLP_CUDA(cudaGetLastError());
 }
 
+namespace {
+// Launch with programmatic stream serialization (PDL): the kernel may begin
+// its static-data prologue while the previous kernel in the stream drains.
+template <class... P, class... A>
+void launch_pdl(void (*kern)(P...), int grid, size_t smem, cudaStream_t s, A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  PDLP_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...));
+}
+}  // namespace
+
 void launch_dual(const DevCsr& k, const DevIter& it, bool seq, unsigned long long cond,
                  int use_cond, cudaStream_t s) {
   const size_t sm = stream_smem_bytes<DualEpi<false>>();
   cudaGraphConditionalHandle h = static_cast<cudaGraphConditionalHandle>(cond);
   if (seq)
-    dual_kernel<true><<<k.ntiles, kThreads, sm, s>>>(k, it, h, use_cond);
+    launch_pdl(dual_kernel<true>, k.ntiles, sm, s, k, it, h, use_cond);
   else
-    dual_kernel<false><<<k.ntiles, kThreads, sm, s>>>(k, it, h, use_cond);
-  PDLP_CUDA(cudaGetLastError());
+    launch_pdl(dual_kernel<false>, k.ntiles, sm, s, k, it, h, use_cond);
 }
 
 void launch_primal(const DevCsr& kt, const DevIter& it, bool seq, int mode_override,
-                   cudaStream_t s) {
-  const size_t sm = stream_smem_bytes<PrimalEpi<false>>();
-  if (seq)
-    primal_kernel<true><<<it.p_grid, kThreads, sm, s>>>(kt, it, mode_override);
-  else
-    primal_kernel<false><<<it.p_grid, kThreads, sm, s>>>(kt, it, mode_override);
-  PDLP_CUDA(cudaGetLastError());
+                   cudaStream_t s, unsigned long long cond, int use_cond) {
+  cudaGraphConditionalHandle h = static_cast<cudaGraphConditionalHandle>(cond);
+  const size_t sm = stream_smem_bytes<PrimalEpi<false, false>>();
+  if (seq) {
+    if (it.nonneg)
+      launch_pdl(primal_kernel<true, true>, it.p_grid, sm, s, kt, it, mode_override, h, use_cond);
+    else
+      launch_pdl(primal_kernel<true, false>, it.p_grid, sm, s, kt, it, mode_override, h, use_cond);
+  } else {
+    if (it.nonneg)
+      launch_pdl(primal_kernel<false, true>, it.p_grid, sm, s, kt, it, mode_override, h, use_cond);
+    else
+      launch_pdl(primal_kernel<false, false>, it.p_grid, sm, s, kt, it, mode_override, h, use_cond);
+  }
 }
 
 void launch_zero_iterate(const DevIter& it, cudaStream_t s) {

@@ -50,7 +50,7 @@ void launch_dual(const DevCsr& k, const DevIter& it, bool seq, unsigned long lon
                  int use_cond, cudaStream_t s);
 // Primal side: K'y' + average + next trial x' (mode from state, or forced).
 void launch_primal(const DevCsr& kt, const DevIter& it, bool seq, int mode_override,
-                   cudaStream_t s);
+                   cudaStream_t s, unsigned long long cond = 0, int use_cond = 0);
 void launch_zero_iterate(const DevIter& it, cudaStream_t s);
 void launch_restart_copy(const DevIter& it, int from_avg, cudaStream_t s);
 

@@ -20,6 +20,7 @@
 
 #include "kernels.cuh"
 #include "solver.cuh"
+#include "window.cuh"
 
 namespace pdlp {
 
@@ -72,6 +73,8 @@ Solver::Solver(const pdlp_lp& lp, const pdlp_params& params) : params_(params) {
 Solver::~Solver() {
   if (ev_begin_) cudaEventDestroy(ev_begin_);
   if (ev_end_) cudaEventDestroy(ev_end_);
+  if (ev_w0_) cudaEventDestroy(ev_w0_);
+  if (ev_w1_) cudaEventDestroy(ev_w1_);
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
   if (graph_) cudaGraphDestroy(graph_);
   if (stream_) cudaStreamDestroy(stream_);
@@ -135,7 +138,8 @@ void Solver::setup(const pdlp_lp& lp) {
 
   cudaStream_t s = stream_;
   // ---- K = vstack(G, A) (sparse_matrix.hpp:181-200) in HBM, int32 indices ----
-  k_rp_.alloc(m_ + 1);
+  k_rp_.alloc(m_ + 1 + kVecPad);  // padded: the window kernel copies quad-aligned spans
+  k_rp_.zero(s);
   k_col_.alloc(nnz_ + kVecPad);
   k_val_orig_.alloc(nnz_ + kVecPad);
   k_val_.alloc(nnz_ + kVecPad);
@@ -203,47 +207,47 @@ void Solver::setup(const pdlp_lp& lp) {
   PDLP_CUDA(cudaStreamSynchronize(s));
   K_ = DevCsr{k_rp_.get(), k_col_.get(), k_val_.get(), k_val_orig_.get(), int(m_), int(n_), nnz_};
   KT_ = DevCsr{kt_rp_.get(), kt_col_.get(), kt_val_.get(), kt_val_orig_.get(), int(n_), int(m_), nnz_};
-  // planner thresholds (env overrides are a tuning aid; defaults in common.cuh)
-  auto knob = [](const char* name, int def) {
-    const char* v = std::getenv(name);
-    return v ? std::atoi(v) : def;
-  };
-  const int smax = std::min(knob("PDLP_STREAM_MAX_ROW", kStreamMaxRow), kStreamNnz);
-  const int wmax = knob("PDLP_WARP_MAX_ROW", kWarpMaxRow);
-  const int cnnz = knob("PDLP_CHUNK_NNZ", kChunkNnz);
-  const int srows = std::min(knob("PDLP_STREAM_ROWS", kStreamRows), kStreamNnz);
-  k_plan_ = plan_tiles<int>(m_, rp_h.data(), parity(), smax, wmax, cnnz, kStreamNnz, srows, kThreads);
-  kt_plan_ = plan_tiles<int>(n_, rpt_h.data(), parity(), smax, wmax, cnnz, kStreamNnz, srows, kThreads);
-  plan(K_, rp_h, k_plan_.tiles, k_tiles_, k_chunk_, k_ctr_);
-  plan(KT_, rpt_h, kt_plan_.tiles, kt_tiles_, kt_chunk_, kt_ctr_);
-  K_.chunk_slots = k_plan_.chunk_slots;
-  KT_.chunk_slots = kt_plan_.chunk_slots;
-  {
-    // chunk counters sized by split rows
-    k_ctr_.alloc(std::max(1, k_plan_.split_rows));
-    k_ctr_.zero(s);
-    kt_ctr_.alloc(std::max(1, kt_plan_.split_rows));
-    kt_ctr_.zero(s);
-    K_.chunk_ctr = k_ctr_.get();
-    KT_.chunk_ctr = kt_ctr_.get();
-  }
+  // three tilings of each operator: iteration kernels, persistent window
+  // kernel, evaluation kernels (common.cuh TileGeom)
+  build_plan(k_it_, K_, rp_h, kIterGeom);
+  build_plan(kt_it_, KT_, rpt_h, kIterGeom);
+  build_plan(k_win_, K_, rp_h, kWinGeom);
+  build_plan(kt_win_, KT_, rpt_h, kWinGeom);
+  build_plan(k_ev_, K_, rp_h, kEvalGeom);
+  build_plan(kt_ev_, KT_, rpt_h, kEvalGeom);
+  K_ = k_it_.csr;
+  KT_ = kt_it_.csr;
 
   allocate_iteration();
   set_kernel_attributes();
 }
 
-void Solver::plan(DevCsr& a, const std::vector<int>&, std::vector<Tile>& tiles_host,
-                  DevBuf<Tile>& tiles, DevBuf<double>& chunk_part, DevBuf<unsigned>&) {
-  tiles.alloc(tiles_host.size());
-  PDLP_CUDA(cudaMemcpyAsync(tiles.get(), tiles_host.data(), tiles_host.size() * sizeof(Tile),
+void Solver::build_plan(OpPlan& p, const DevCsr& base, const std::vector<int>& rp,
+                        const TileGeom& g) {
+  // planner thresholds: env overrides are a tuning aid (clamped to the geometry)
+  auto knob = [](const char* name, int def) {
+    const char* v = std::getenv(name);
+    return v ? std::atoi(v) : def;
+  };
+  const int smax = std::min(knob("PDLP_STREAM_MAX_ROW", kStreamMaxRow), g.stream_nnz);
+  const int wmax = std::min(knob("PDLP_WARP_MAX_ROW", kWarpMaxRow), g.lane_nnz * kThreads);
+  const int cnnz = std::min(knob("PDLP_CHUNK_NNZ", g.chunk_nnz), g.chunk_nnz);
+  const int lane = std::min(knob("PDLP_LANE_NNZ", g.lane_nnz), g.lane_nnz);
+  p.plan = plan_tiles<int>(int64_t(rp.size()) - 1, rp.data(), parity(), smax, wmax, cnnz,
+                           g.stream_nnz, g.stream_rows, kThreads, lane);
+  const std::vector<Tile>& th = p.plan.tiles;
+  p.tiles.alloc(th.size());
+  PDLP_CUDA(cudaMemcpyAsync(p.tiles.get(), th.data(), th.size() * sizeof(Tile),
                             cudaMemcpyHostToDevice, stream_));
-  int slots = 0;
-  for (const Tile& t : tiles_host)
-    if (t.kind == kTileChunk && t.nparts > 1) slots = std::max(slots, t.slot + t.nparts);
-  chunk_part.alloc(size_t(std::max(1, slots)) * 8);
-  a.tiles = tiles.get();
-  a.ntiles = int(tiles_host.size());
-  a.chunk_part = chunk_part.get();
+  p.chunk.alloc(size_t(std::max(1, p.plan.chunk_slots)) * 8);
+  p.ctr.alloc(std::max(1, p.plan.split_rows));
+  p.ctr.zero(stream_);
+  p.csr = base;
+  p.csr.tiles = p.tiles.get();
+  p.csr.ntiles = int(th.size());
+  p.csr.chunk_slots = p.plan.chunk_slots;
+  p.csr.chunk_part = p.chunk.get();
+  p.csr.chunk_ctr = p.ctr.get();
 }
 
 // explicit_transpose (sparse_matrix.hpp:167-178) on the device: a stable LSD
@@ -251,7 +255,8 @@ void Solver::plan(DevCsr& a, const std::vector<int>&, std::vector<Tile>& tiles_h
 // row order, i.e. the reference's CSR of K^T; integer output is exact.
 void Solver::build_transpose() {
   cudaStream_t s = stream_;
-  kt_rp_.alloc(n_ + 1);
+  kt_rp_.alloc(n_ + 1 + kVecPad);
+  kt_rp_.zero(s);
   kt_col_.alloc(nnz_ + kVecPad);
   kt_val_orig_.alloc(nnz_ + kVecPad);
   kt_val_.alloc(nnz_ + kVecPad);
@@ -364,7 +369,7 @@ void Solver::allocate_iteration() {
   const int avg_blocks = std::max<int64_t>(1, (m_ + 4095) / 4096);
   const int p_grid = KT_.ntiles + avg_blocks;
   d_part_.alloc(size_t(K_.ntiles) * 3);
-  p_part_.alloc(size_t(p_grid) * 2);
+  p_part_.alloc(size_t(p_grid) * 4 + 2);  // two parity buffers
   p_part_.zero(s);
   const bool seq = parity();
   seq_dy2_.alloc(seq ? m_ : 1);
@@ -375,6 +380,8 @@ void Solver::allocate_iteration() {
   gro_tab_.alloc(tab_cap_);
   step_log_dev_.alloc(tab_cap_);
   state_dev_.alloc(1);
+  snap_dev_.alloc(1);
+  snap_dev_.zero(s);
   state_dev_.zero(s);
   hs_.alloc(1);
   he_.alloc(1);
@@ -403,15 +410,42 @@ void Solver::allocate_iteration() {
   it.m = int(m_);
   it.m1 = int(m1_);
   it.p_grid = p_grid;
+  {
+    // l = +0 (sign bit clear, so l / d2 stays +0) and u = +inf everywhere:
+    // min(max(v, l), u) == max(v, 0) bitwise, and the bound streams are skipped
+    bool nonneg = true;
+    for (int64_t j = 0; j < n_ && nonneg; ++j)
+      nonneg = l_[j] == 0.0 && !std::signbit(l_[j]) && u_[j] == INFINITY;
+    it.nonneg = nonneg ? 1 : 0;
+  }
   it.avg_blocks = avg_blocks;
   it.d_part = d_part_.get();
   it.p_part = p_part_.get();
+  it.px_total = p_part_.get() + size_t(p_grid) * 4;
+  it.snap = snap_dev_.get();
+  it.d_tiles = K_.ntiles;
   it.seq_dy2 = seq_dy2_.get();
   it.seq_inter = seq_inter_.get();
   it.seq_dx2 = seq_dx2_.get();
   it.red_tab = red_tab_.get();
   it.gro_tab = gro_tab_.get();
   it.step_log = step_log_dev_.get();
+  // iteration engine
+  engine_ = params_.engine;
+  if (engine_ == PDLP_ENGINE_AUTO)
+    engine_ = params_.use_cuda_graph ? PDLP_ENGINE_GRAPH : PDLP_ENGINE_STREAM;
+  if (engine_ == PDLP_ENGINE_PERSISTENT && parity())
+    invalid("params: the persistent engine runs fast mode only");
+  if (engine_ == PDLP_ENGINE_PERSISTENT) {
+    win_grid_ = window_grid(params_.device);
+    wd_part_.alloc(size_t(win_grid_) * 3);
+    wp_part_.alloc(size_t(win_grid_) * 2);
+    bar_.alloc(1);
+    bar_.zero(s);
+    wb_.wd_part = wd_part_.get();
+    wb_.wp_part = wp_part_.get();
+    wb_.bar = bar_.get();
+  }
   it.st = state_dev_.get();
 
   X4_.alloc(size_t(n_) * 4);
@@ -420,8 +454,8 @@ void Solver::allocate_iteration() {
   scratch_n_.alloc(n_);
   const int grid0 = eval_grid0(int(n_), int(m_));
   part0_.alloc(size_t(std::max(1, grid0)) * 4);
-  part1_.alloc(size_t(K_.ntiles) * 14);
-  part2_.alloc(size_t(KT_.ntiles) * 18);
+  part1_.alloc(size_t(k_ev_.csr.ntiles) * 14);
+  part2_.alloc(size_t(kt_ev_.csr.ntiles) * 18);
   seq_r_.alloc(seq ? size_t(m_) * 4 : 1);
   seq_d_.alloc(seq ? size_t(n_) * 4 : 1);
   eval_dev_.alloc(1);
@@ -463,7 +497,7 @@ void Solver::capture_window_graph() {
   PDLP_CUDA(cudaStreamBeginCaptureToGraph(stream_, body, nullptr, nullptr, 0,
                                           cudaStreamCaptureModeThreadLocal));
   launch_dual(K_, it_, parity(), static_cast<unsigned long long>(h), 1, stream_);
-  launch_primal(KT_, it_, parity(), -1, stream_);
+  launch_primal(KT_, it_, parity(), -1, stream_, static_cast<unsigned long long>(h), 1);
   PDLP_CUDA(cudaStreamEndCapture(stream_, &body));
   PDLP_CUDA(cudaGraphInstantiate(&graph_exec_, graph_, 0));
   cond_handle_ = static_cast<unsigned long long>(h);
@@ -511,7 +545,10 @@ void Solver::iterate_begin(int32_t* status) {
   if (!ev_begin_) {
     PDLP_CUDA(cudaEventCreate(&ev_begin_));
     PDLP_CUDA(cudaEventCreate(&ev_end_));
+    PDLP_CUDA(cudaEventCreate(&ev_w0_));
+    PDLP_CUDA(cudaEventCreate(&ev_w1_));
   }
+  window_seconds_ = 0.0;
   PDLP_CUDA(cudaEventRecord(ev_begin_, stream_));
   upload_state();
   launch_zero_iterate(it_, stream_);  // z = 0, Kx = K 0 = 0, K'y = 0 (solver.hpp:764-769)
@@ -528,6 +565,7 @@ void Solver::iterate_begin(int32_t* status) {
     upload_state();
     launch_primal(KT_, it_, parity(), kPRetry, stream_);
     ++launches_;
+    p_from_window_ = false;
   }
   if (status) *status = finished_ ? info_.status : PDLP_STATUS_RUNNING;
 }
@@ -590,9 +628,21 @@ void Solver::run_window(int target) {
   PDLP_CUDA(cudaMemcpyAsync(gro_tab_.get(), gro, target * sizeof(double), cudaMemcpyHostToDevice,
                             stream_));
   upload_state();
-  if (params_.use_cuda_graph) {
+  PDLP_CUDA(cudaEventRecord(ev_w0_, stream_));
+  if (engine_ == PDLP_ENGINE_PERSISTENT) {
+    WinBufs wb = wb_;
+    wb.p_src = p_from_window_ ? wb_.wp_part
+                              : it_.p_part + size_t(st.trials_total & 1) * it_.p_grid * 2;
+    wb.p_src_count = p_from_window_ ? win_grid_ : it_.p_grid;
+    launch_window(k_win_.csr, kt_win_.csr, it_, wb, win_grid_, stream_);
+    PDLP_CUDA(cudaEventRecord(ev_w1_, stream_));
+    download_state();
+    p_from_window_ = true;
+    launches_ += 1;
+  } else if (engine_ == PDLP_ENGINE_GRAPH) {
     if (!graph_exec_) capture_window_graph();
     PDLP_CUDA(cudaGraphLaunch(graph_exec_, stream_));
+    PDLP_CUDA(cudaEventRecord(ev_w1_, stream_));
     download_state();
   } else {
     int remaining = target;
@@ -601,12 +651,18 @@ void Solver::run_window(int target) {
         launch_dual(K_, it_, parity(), 0, 0, stream_);
         launch_primal(KT_, it_, parity(), -1, stream_);
       }
+      PDLP_CUDA(cudaEventRecord(ev_w1_, stream_));
       download_state();
       if (st.failure || st.window_accepts >= target) break;
       remaining = target - st.window_accepts;
     }
   }
-  launches_ += 2 * (st.trials_total - trials_before);
+  {
+    float ms = 0.f;
+    PDLP_CUDA(cudaEventElapsedTime(&ms, ev_w0_, ev_w1_));
+    window_seconds_ += 1e-3 * double(ms);
+  }
+  if (engine_ != PDLP_ENGINE_PERSISTENT) launches_ += 2 * (st.trials_total - trials_before);
   if (st.record_log && st.window_accepts > 0) {
     PDLP_CUDA(cudaMemcpyAsync(log_host_.get(), step_log_dev_.get(),
                               st.window_accepts * sizeof(pdlp_step_log_entry),
@@ -618,7 +674,7 @@ void Solver::run_window(int target) {
 
 void Solver::evaluate() {
   upload_state();
-  launch_eval(K_, KT_, it_, ev_, parity(), stream_);
+  launch_eval(k_ev_.csr, kt_ev_.csr, it_, ev_, parity(), stream_);
   launches_ += parity() ? 5 : 4;
   ++evaluations_;
   PDLP_CUDA(cudaMemcpyAsync(he_.get(), eval_dev_.get(), sizeof(EvalOut), cudaMemcpyDeviceToHost,
@@ -717,6 +773,7 @@ void Solver::evaluation_block() {
   launch_spmv(K_, false, it_.x[st.ix_cur], it_.kx[st.ikx_cur], parity(), stream_);
   launch_primal(KT_, it_, parity(), kPRestart, stream_);
   launches_ += 3;
+  p_from_window_ = false;
   ev.omega_after = st.omega;
   restart_log_.push_back(ev);
   kkt_epoch_start_ = rc.weighted(st.omega);
@@ -782,6 +839,7 @@ void Solver::finish(int status, int slot_x, int slot_y, int slot_lam, const KktH
     float ms = 0.f;
     PDLP_CUDA(cudaEventElapsedTime(&ms, ev_begin_, ev_end_));
     in.device_seconds = 1e-3 * double(ms);
+    in.window_seconds = window_seconds_;
   }
   in.step_log_size = int64_t(step_log_.size());
   in.restart_log_size = int64_t(restart_log_.size());
@@ -880,6 +938,34 @@ void Solver::time_kernel(int which, int reps, double* avg_ms, double* bytes) {
   if (!begun_) {
     int32_t s;
     iterate_begin(&s);
+  }
+  if (which == 2 || which == 3) {
+    // plain SpMV microbenchmark on device-resident vectors: 2 = K x, 3 = K^T y
+    const DevState& st = *hs_.get();
+    cudaEvent_t e0, e1;
+    PDLP_CUDA(cudaEventCreate(&e0));
+    PDLP_CUDA(cudaEventCreate(&e1));
+    auto run = [&]() {
+      if (which == 2)
+        launch_spmv(K_, false, it_.x[st.ix_cur], it_.kx[1 - st.ikx_cur], parity(), stream_);
+      else
+        launch_spmv(KT_, false, it_.y[st.iy_cur], it_.kty[1 - st.ikty_cur], parity(), stream_);
+    };
+    run();
+    PDLP_CUDA(cudaEventRecord(e0, stream_));
+    for (int r = 0; r < reps; ++r) run();
+    PDLP_CUDA(cudaEventRecord(e1, stream_));
+    PDLP_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    PDLP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (avg_ms) *avg_ms = ms / reps;
+    const double nnz = double(nnz_), rows = double(which == 2 ? m_ : n_),
+                 cols = double(which == 2 ? n_ : m_);
+    if (bytes) *bytes = 12.0 * nnz + 4.0 * (rows + 1) + 8.0 * cols + 8.0 * rows;
+    state_valid_ = false;
+    return;
   }
   reps = std::max(1, std::min(reps, tab_cap_));
   DevState& st = *hs_.get();

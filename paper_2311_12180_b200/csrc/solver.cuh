@@ -11,6 +11,7 @@
 #include "common.cuh"
 #include "device_state.h"
 #include "tiles.h"
+#include "window.cuh"
 
 namespace pdlp {
 
@@ -102,8 +103,14 @@ class Solver {
   void setup(const pdlp_lp& lp);
   void build_transpose();
   void precondition();
-  void plan(DevCsr& a, const std::vector<int>& rp_host, std::vector<Tile>& tiles_host,
-            DevBuf<Tile>& tiles, DevBuf<double>& chunk_part, DevBuf<unsigned>& chunk_ctr);
+  struct OpPlan {
+    TilePlan plan;
+    DevBuf<Tile> tiles;
+    DevBuf<double> chunk;
+    DevBuf<unsigned> ctr;
+    DevCsr csr{};
+  };
+  void build_plan(OpPlan& p, const DevCsr& base, const std::vector<int>& rp, const TileGeom& g);
   void allocate_iteration();
   void capture_window_graph();
   void upload_state();
@@ -132,11 +139,8 @@ class Solver {
   // operator storage: K = (G; A) and its separately stored transpose
   DevBuf<int> k_rp_, k_col_, kt_rp_, kt_col_;
   DevBuf<double> k_val_, k_val_orig_, kt_val_, kt_val_orig_;
-  DevBuf<Tile> k_tiles_, kt_tiles_;
-  DevBuf<double> k_chunk_, kt_chunk_;
-  DevBuf<unsigned> k_ctr_, kt_ctr_;
-  TilePlan k_plan_, kt_plan_;
-  DevCsr K_{}, KT_{};
+  OpPlan k_it_, kt_it_, k_win_, kt_win_, k_ev_, kt_ev_;
+  DevCsr K_{}, KT_{};  // the iteration-kernel tilings
 
   // vectors
   DevBuf<double> c_orig_, l_orig_, u_orig_, q_orig_, d1_dev_, d2_dev_;
@@ -145,7 +149,7 @@ class Solver {
   DevBuf<double> d_part_, p_part_, seq_dy2_, seq_inter_, seq_dx2_;
   DevBuf<double> red_tab_, gro_tab_;
   DevBuf<pdlp_step_log_entry> step_log_dev_;
-  DevBuf<DevState> state_dev_;
+  DevBuf<DevState> state_dev_, snap_dev_;
   DevBuf<double> X4_, Y4_, lam_, part0_, part1_, part2_, seq_r_, seq_d_, scratch_n_, scratch_m_;
   DevBuf<EvalOut> eval_dev_;
   DevIter it_{};
@@ -168,7 +172,15 @@ class Solver {
   bool begun_ = false, finished_ = false, state_valid_ = false;
   int64_t launches_ = 0, evaluations_ = 0;
   double setup_seconds_ = 0.0;
-  cudaEvent_t ev_begin_ = nullptr, ev_end_ = nullptr;
+  cudaEvent_t ev_begin_ = nullptr, ev_end_ = nullptr, ev_w0_ = nullptr, ev_w1_ = nullptr;
+  double window_seconds_ = 0.0;
+  // persistent window engine
+  int engine_ = PDLP_ENGINE_PERSISTENT;
+  int win_grid_ = 0;
+  bool p_from_window_ = false;
+  DevBuf<double> wd_part_, wp_part_;
+  DevBuf<GridBar> bar_;
+  WinBufs wb_{};
   std::vector<pdlp_step_log_entry> step_log_;
   std::vector<pdlp_restart_event> restart_log_;
   pdlp_result_info info_{};

@@ -22,8 +22,8 @@ namespace pdlp {
 
 template <class Epi>
 constexpr size_t stream_smem_bytes() {
-  return size_t(kStreamNnz) * Epi::NP * sizeof(double) +
-         (Epi::kNeedCol ? size_t(kStreamNnz) * sizeof(int) : 0) + 64;
+  return size_t(Epi::kGeom.stream_nnz) * Epi::NP * sizeof(double) +
+         (Epi::kNeedCol ? size_t(Epi::kGeom.stream_nnz) * sizeof(int) : 0) + 64;
 }
 
 template <class Epi>
@@ -49,33 +49,90 @@ __device__ __forceinline__ void row_sum_sequential(const Epi& epi, const int* __
   }
 }
 
+// CRTP base: the default group epilogue hands each row to row_done. Epilogues
+// that touch several dense arrays per row override rows_done to use 128-bit
+// loads over the 4 consecutive rows one thread owns in a STREAM tile.
+template <class D>
+struct EpiBase {
+  template <int NA, int NR>
+  __device__ __forceinline__ void rows_done(int r0, int nr, const double (&acc)[4][NA],
+                                            double (&red)[NR]) const {
+    for (int i = 0; i < nr; ++i) static_cast<const D*>(this)->row_done(r0 + i, acc[i], red);
+  }
+};
+
+// Loads in flight per lane: 2 quads (8 nnz) per batch for the scalar-gather kernels.
+template <class Epi>
+__host__ __device__ constexpr int quad_unroll() { return Epi::NP == 1 ? 2 : 1; }
+
 // Strided partial sum over [k0, k1) by `nthreads` threads with lane index `t`,
-// using aligned 128-bit loads of indices and values.
+// using aligned 128-bit loads of indices and values; U quads of index/value
+// loads are issued before their gathers so each lane keeps ~3U+4U requests in
+// flight. Each lane accumulates its quads in increasing order (deterministic).
 template <class Epi>
 __device__ __forceinline__ void strided_partial(const Epi& epi, const int* __restrict__ col,
                                                 const double* __restrict__ val, int k0, int k1,
                                                 int t, int nthreads, double (&acc)[Epi::NA]) {
+  constexpr int U = quad_unroll<Epi>();
   zero_acc<Epi>(acc);
   const int base = k0 & ~3;
   const int nq = (k1 - base + 3) >> 2;
-  for (int q = t; q < nq; q += nthreads) {
-    const int k = base + 4 * q;
-    const int4 c4 = ld_stream_i4(col + k);
-    const double2 va = ld_stream_d2(val + k);
-    const double2 vb = ld_stream_d2(val + k + 2);
-    const int cs[4] = {c4.x, c4.y, c4.z, c4.w};
-    const double vs[4] = {va.x, va.y, vb.x, vb.y};
+  for (int q0 = t; q0 < nq; q0 += nthreads * U) {
+    int cs[U][4];
+    double vs[U][4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int e = k + i;
-      if (e >= k0 && e < k1) {
-        double g[Epi::NP], p[Epi::NP];
-        epi.gather(cs[i], g);
+    for (int u = 0; u < U; ++u) {
+      const int q = q0 + u * nthreads;
+      if (q < nq) {
+        const int k = base + 4 * q;
+        const int4 c4 = ld_stream_i4(col + k);
+        const double2 va = ld_stream_d2(val + k);
+        const double2 vb = ld_stream_d2(val + k + 2);
+        cs[u][0] = c4.x, cs[u][1] = c4.y, cs[u][2] = c4.z, cs[u][3] = c4.w;
+        vs[u][0] = va.x, vs[u][1] = va.y, vs[u][2] = vb.x, vs[u][3] = vb.y;
+      } else {
 #pragma unroll
-        for (int j = 0; j < Epi::NP; ++j) p[j] = vs[i] * g[j];
-        epi.add(acc, p, cs[i]);
+        for (int i = 0; i < 4; ++i) cs[u][i] = 0, vs[u][i] = 0.0;
       }
     }
+    double g[U][4][Epi::NP];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = base + 4 * (q0 + u * nthreads);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int e = k + i;
+        if (e >= k0 && e < k1) epi.gather(cs[u][i], g[u][i]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = base + 4 * (q0 + u * nthreads);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int e = k + i;
+        if (e >= k0 && e < k1) {
+          double p[Epi::NP];
+#pragma unroll
+          for (int j = 0; j < Epi::NP; ++j) p[j] = vs[u][i] * g[u][i][j];
+          epi.add(acc, p, cs[u][i]);
+        }
+      }
+    }
+  }
+}
+
+// Pulls a tile's static operator data (offsets, indices, values) toward L2
+// before griddep_wait(), so the loads after it overlap the predecessor's tail.
+__device__ __forceinline__ void prefetch_tile(const Tile& t, const int* rp, const int* col,
+                                              const double* val) {
+  const int k0 = t.k0 & ~31, k1 = t.k1;
+  // 128-byte lines: 32 indices or 16 values per line
+  for (int k = k0 + 32 * int(threadIdx.x); k < k1; k += 32 * kThreads) prefetch_l2(col + k);
+  for (int k = (t.k0 & ~15) + 16 * int(threadIdx.x); k < k1; k += 16 * kThreads) prefetch_l2(val + k);
+  if (t.kind != kTileChunk) {
+    const int r = (t.row0 & ~31) + 32 * int(threadIdx.x);
+    if (r <= t.row1) prefetch_l2(rp + r);
   }
 }
 
@@ -87,59 +144,129 @@ __device__ void run_tile(const Tile& t, const int* __restrict__ rp, const int* _
                          double* chunk_part, unsigned* chunk_ctr, unsigned char* smem) {
   const int tid = threadIdx.x;
   if (t.kind == kTileStream) {
+    constexpr int U = quad_unroll<Epi>() > 2 ? 2 : quad_unroll<Epi>();
     double* sprod = reinterpret_cast<double*>(smem);
-    int* scol = reinterpret_cast<int*>(sprod + size_t(kStreamNnz) * Epi::NP);
+    int* scol = reinterpret_cast<int*>(sprod + size_t(Epi::kGeom.stream_nnz) * Epi::NP);
     const int base = t.k0 & ~3;
     const int nq = (t.k1 - base + 3) >> 2;
-    for (int q = tid; q < nq; q += kThreads) {
-      const int k = base + 4 * q;
-      const int4 c4 = ld_stream_i4(col + k);
-      const double2 va = ld_stream_d2(val + k);
-      const double2 vb = ld_stream_d2(val + k + 2);
-      const int cs[4] = {c4.x, c4.y, c4.z, c4.w};
-      const double vs[4] = {va.x, va.y, vb.x, vb.y};
+    for (int q0 = tid; q0 < nq; q0 += kThreads * U) {
+      int cs[U][4];
+      double vs[U][4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int e = k + i;
-        if (e >= t.k0 && e < t.k1) {
-          double g[Epi::NP];
-          epi.gather(cs[i], g);
-          const int s = e - t.k0;
+      for (int u = 0; u < U; ++u) {
+        const int q = q0 + u * kThreads;
+        if (q < nq) {
+          const int k = base + 4 * q;
+          const int4 c4 = ld_stream_i4(col + k);
+          const double2 va = ld_stream_d2(val + k);
+          const double2 vb = ld_stream_d2(val + k + 2);
+          cs[u][0] = c4.x, cs[u][1] = c4.y, cs[u][2] = c4.z, cs[u][3] = c4.w;
+          vs[u][0] = va.x, vs[u][1] = va.y, vs[u][2] = vb.x, vs[u][3] = vb.y;
+        } else {
 #pragma unroll
-          for (int j = 0; j < Epi::NP; ++j) sprod[size_t(s) * Epi::NP + j] = vs[i] * g[j];
-          if (Epi::kNeedCol) scol[s] = cs[i];
+          for (int i = 0; i < 4; ++i) cs[u][i] = 0, vs[u][i] = 0.0;
+        }
+      }
+      double g[U][4][Epi::NP];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = base + 4 * (q0 + u * kThreads);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int e = k + i;
+          if (e >= t.k0 && e < t.k1) epi.gather(cs[u][i], g[u][i]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = base + 4 * (q0 + u * kThreads);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int e = k + i;
+          if (e >= t.k0 && e < t.k1) {
+            const int s = e - t.k0;
+#pragma unroll
+            for (int j = 0; j < Epi::NP; ++j) sprod[size_t(s) * Epi::NP + j] = vs[u][i] * g[u][i][j];
+            if (Epi::kNeedCol) scol[s] = cs[u][i];
+          }
         }
       }
     }
     __syncthreads();
-    for (int r = t.row0 + tid; r < t.row1; r += kThreads) {
-      const int a = rp[r] - t.k0, b = rp[r + 1] - t.k0;
-      double acc[Epi::NA];
-      zero_acc<Epi>(acc);
-      for (int s = a; s < b; ++s) {
-        double p[Epi::NP];
+    // each thread owns groups of 4 consecutive rows and sums each row in index
+    // order from the staged products
+    constexpr int kGroups = Epi::kGeom.stream_rows / (4 * kThreads);
 #pragma unroll
-        for (int j = 0; j < Epi::NP; ++j) p[j] = sprod[size_t(s) * Epi::NP + j];
-        epi.add(acc, p, Epi::kNeedCol ? scol[s] : 0);
+    for (int gi = 0; gi < kGroups; ++gi) {
+      const int r0 = t.row0 + 4 * (tid + gi * kThreads);
+      if (r0 >= t.row1) break;
+      const int nr = min(4, t.row1 - r0);
+      int bounds[5];
+#pragma unroll
+      for (int i = 0; i < 5; ++i) bounds[i] = i <= nr ? rp[r0 + i] - t.k0 : 0;
+      double acc[4][Epi::NA];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+#pragma unroll
+        for (int j = 0; j < Epi::NA; ++j) acc[i][j] = 0.0;
+        if (i < nr) {
+          for (int s = bounds[i]; s < bounds[i + 1]; ++s) {
+            double p[Epi::NP];
+#pragma unroll
+            for (int j = 0; j < Epi::NP; ++j) p[j] = sprod[size_t(s) * Epi::NP + j];
+            epi.add(acc[i], p, Epi::kNeedCol ? scol[s] : 0);
+          }
+        }
       }
-      epi.row_done(r, acc, red);
+      epi.rows_done(r0, nr, acc, red);
     }
     __syncthreads();
   } else if (t.kind == kTileWarp) {
-    const int warp = tid >> 5, lane = tid & 31;
-    const int r = t.row0 + warp;
+    // G lanes per row (t.part in {8,...,256}, ~8 nnz per lane: one batch of
+    // loads), kThreads / G rows per tile; lane partials combine by a fixed
+    // butterfly inside the warp, then warps of a group in warp order.
+    const int G = t.part;
+    const int grp = tid / G, lane = tid % G;
+    const int r = t.row0 + grp;
+    double acc[Epi::NA];
+    zero_acc<Epi>(acc);
     if (r < t.row1) {
       const int k0 = rp[r], k1 = rp[r + 1];
-      double acc[Epi::NA];
       if (kSeq) {
         if (lane == 0) row_sum_sequential(epi, col, val, k0, k1, acc);
       } else {
-        strided_partial(epi, col, val, k0, k1, lane, 32, acc);
-#pragma unroll
-        for (int i = 0; i < Epi::NA; ++i) acc[i] = warp_sum(acc[i]);
+        strided_partial(epi, col, val, k0, k1, lane, G, acc);
       }
-      if (lane == 0) epi.row_done(r, acc, red);
     }
+    if (!kSeq) {
+      const int width = G < 32 ? G : 32;
+#pragma unroll
+      for (int i = 0; i < Epi::NA; ++i) {
+        double v = acc[i];
+        for (int o = width >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        acc[i] = v;
+      }
+      if (G > 32) {
+        __shared__ double sgrp[kWarps * Epi::NA];
+        const int warp = tid >> 5;
+        if ((tid & 31) == 0) {
+#pragma unroll
+          for (int i = 0; i < Epi::NA; ++i) sgrp[warp * Epi::NA + i] = acc[i];
+        }
+        __syncthreads();
+        if (lane == 0) {
+          const int w0 = warp, nw = G / 32;
+#pragma unroll
+          for (int i = 0; i < Epi::NA; ++i) {
+            double v = sgrp[w0 * Epi::NA + i];
+            for (int w = 1; w < nw; ++w) v += sgrp[(w0 + w) * Epi::NA + i];
+            acc[i] = v;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    if (lane == 0 && r < t.row1) epi.row_done(r, acc, red);
   } else {  // kTileChunk
     __shared__ double sred[kWarps * Epi::NA];
     __shared__ bool last_part;
@@ -193,9 +320,11 @@ __device__ __forceinline__ void store_partial(double (&red)[NS + NM], double* pa
 // Grid-level "am I the last CTA" ticket; resets the counter for the next replay.
 __device__ __forceinline__ bool grid_last_block(unsigned* counter, unsigned total) {
   __shared__ bool is_last;
-  __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
+    // thread 0 wrote this CTA's partial; publish it before taking a ticket (a
+    // fence in every thread would also flush every SM's L1 on sm_100)
+    __threadfence();
     const unsigned t = atomicAdd(counter, 1u);
     is_last = (t == total - 1u);
     if (is_last) *counter = 0u;

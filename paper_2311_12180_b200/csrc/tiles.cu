@@ -7,7 +7,8 @@ namespace pdlp {
 
 template <class Off>
 TilePlan plan_tiles(int64_t rows, const Off* rp, bool parity, int stream_max_row,
-                    int warp_max_row, int chunk_nnz, int stream_nnz, int stream_rows, int threads) {
+                    int warp_max_row, int chunk_nnz, int stream_nnz, int stream_rows, int threads,
+                    int lane_nnz) {
   TilePlan plan;
   int64_t r = 0;
   auto len = [&](int64_t i) { return int64_t(rp[i + 1] - rp[i]); };
@@ -18,13 +19,24 @@ TilePlan plan_tiles(int64_t rows, const Off* rp, bool parity, int stream_max_row
       while (r < rows && r - r0 < stream_rows && len(r) <= stream_max_row &&
              int64_t(rp[r + 1]) - k0 <= stream_nnz)
         ++r;
+      // end interior tiles on a multiple of 4 rows so the 4-row groups of the
+      // next tile stay 32-byte aligned for vector epilogues
+      if (r < rows && r - r0 > 4 && (r & 3) && len(r) <= stream_max_row) r -= (r & 3);
       plan.tiles.push_back({kTileStream, int32_t(r0), int32_t(r), int32_t(k0), int32_t(rp[r]), 0, 1, 0});
       ++plan.stream_tiles;
     } else if (!parity && l <= warp_max_row) {
+      // lanes per row: ~lane_nnz per lane, a power of two in [8, threads]
+      auto lanes = [&](int64_t L) {
+        int64_t g = 8;
+        while (g < threads && g * lane_nnz < L) g *= 2;
+        return int(g);
+      };
+      const int g = lanes(l);
       const int64_t r0 = r;
-      const int warps = threads / 32;
-      while (r < rows && r - r0 < warps && len(r) > stream_max_row && len(r) <= warp_max_row) ++r;
-      plan.tiles.push_back({kTileWarp, int32_t(r0), int32_t(r), int32_t(rp[r0]), int32_t(rp[r]), 0, 1, 0});
+      while (r < rows && r - r0 < threads / g && len(r) > stream_max_row && len(r) <= warp_max_row &&
+             lanes(len(r)) == g)
+        ++r;
+      plan.tiles.push_back({kTileWarp, int32_t(r0), int32_t(r), int32_t(rp[r0]), int32_t(rp[r]), g, 1, 0});
       ++plan.warp_tiles;
     } else {
       const int64_t k0 = rp[r], k1 = rp[r + 1];
@@ -50,7 +62,8 @@ TilePlan plan_tiles(int64_t rows, const Off* rp, bool parity, int stream_max_row
   return plan;
 }
 
-template TilePlan plan_tiles<int>(int64_t, const int*, bool, int, int, int, int, int, int);
-template TilePlan plan_tiles<int64_t>(int64_t, const int64_t*, bool, int, int, int, int, int, int);
+template TilePlan plan_tiles<int>(int64_t, const int*, bool, int, int, int, int, int, int, int);
+template TilePlan plan_tiles<int64_t>(int64_t, const int64_t*, bool, int, int, int, int, int, int,
+                                      int);
 
 }  // namespace pdlp

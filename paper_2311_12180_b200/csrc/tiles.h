@@ -6,7 +6,8 @@
 //           the gathered products are staged in shared memory, and each row is then
 //           summed by one thread in index order — the reference's sequential order
 //           (sparse_matrix.hpp:123-131), so STREAM rows are bitwise equal to it;
-//   WARP    up to 8 medium rows, one warp per row, fixed butterfly reduction;
+//   WARP    medium rows, G lanes per row (G = 8..256 chosen for ~lane_nnz per lane,
+//           stored in Tile::part), kThreads/G rows per tile, fixed-order reduction;
 //   CHUNK   one long row or a kChunkNnz slice of it (merge-path style split for
 //           skewed rows, e.g. the multicommodity budget rows); slices combine their
 //           partials in slice order in whichever CTA finishes last (deterministic).
@@ -45,6 +46,7 @@ struct TilePlan {
 // `parity` disables WARP tiles and row splitting.
 template <class Off>
 TilePlan plan_tiles(int64_t rows, const Off* rp, bool parity, int stream_max_row,
-                    int warp_max_row, int chunk_nnz, int stream_nnz, int stream_rows, int threads);
+                    int warp_max_row, int chunk_nnz, int stream_nnz, int stream_rows, int threads,
+                    int lane_nnz);
 
 }  // namespace pdlp

@@ -233,6 +233,7 @@ class SolverParams:
     mode: Mode = Mode.FAST
     use_cuda_graph: bool = True
     l2_persist: bool = True
+    engine: int = 0  # abi.ENGINE_*: AUTO picks the persistent window kernel in fast mode
 
     def validate(self) -> None:
         """SolverParams::validate (solver.hpp:79-93)."""
