@@ -41,7 +41,7 @@ struct TileGeom {
   int lane_nnz;    // target nnz per lane in WARP tiles
   int chunk_nnz;   // nnz per CHUNK tile of a split row
 };
-constexpr TileGeom kIterGeom{4096, 2048, 16, 4096};
+constexpr TileGeom kIterGeom{4096, 1024, 16, 4096};
 constexpr TileGeom kWinGeom{2048, 1024, 8, 2048};
 constexpr TileGeom kEvalGeom{1024, 1024, 8, 2048};
 constexpr int kStreamNnz = 4096;     // largest STREAM tile of any geometry

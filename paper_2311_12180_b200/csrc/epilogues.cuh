@@ -80,6 +80,40 @@ struct DualEpi : EpiBase<DualEpi<kSeq, kCoh>> {
     red[1] += di;
     red[2] += isfinite(yn) ? 0.0 : 1.0;
   }
+  // all operand loads of the thread's rows first, then the updates (ILP)
+  template <int RPT, int NA, int NR>
+  __device__ __forceinline__ void rows_strided(int r0, int stride, int nvalid,
+                                               const double (&acc)[RPT][NA],
+                                               double (&red)[NR]) const {
+    double kxo[RPT], yo[RPT], qq[RPT];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i)
+      if (i < nvalid) {
+        const int r = r0 + i * stride;
+        kxo[i] = ldv<kCoh>(kx + r);
+        yo[i] = ldv<kCoh>(y + r);
+        qq[i] = q[r];
+      }
+#pragma unroll
+    for (int i = 0; i < RPT; ++i)
+      if (i < nvalid) {
+        const int r = r0 + i * stride;
+        const double kxn = acc[i][0];
+        double yn = yo[i] + sigma * (qq[i] - 2.0 * kxn + kxo[i]);  // solver.hpp:412-413
+        if (r < m1 && yn < 0.0) yn = 0.0;
+        yt[r] = yn;
+        kxt[r] = kxn;
+        const double d = yn - yo[i];
+        const double dd = d * d, di = d * (kxn - kxo[i]);
+        if (kSeq) {
+          seq_dy2[r] = dd;
+          seq_inter[r] = di;
+        }
+        red[0] += dd;
+        red[1] += di;
+        red[2] += isfinite(yn) ? 0.0 : 1.0;
+      }
+  }
 };
 
 template <bool kSeq, bool kNonneg, bool kCoh = false>
@@ -156,6 +190,41 @@ struct PrimalEpi : EpiBase<PrimalEpi<kSeq, kNonneg, kCoh>> {
     st2(kty_out + j0, s4);
     st2(xt + j0, xn4);
     if (do_avg) st2(avg_x + j0, av);
+  }
+  // all operand loads of the thread's columns first, then the updates (ILP)
+  template <int RPT, int NA, int NR>
+  __device__ __forceinline__ void rows_strided(int j0, int stride, int nvalid,
+                                               const double (&acc)[RPT][NA],
+                                               double (&red)[NR]) const {
+    double xa[RPT], cc[RPT], av[RPT], ll[RPT], uu[RPT];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i)
+      if (i < nvalid) {
+        const int j = j0 + i * stride;
+        xa[i] = ldv<kCoh>(xc + j);
+        cc[i] = c[j];
+        if (do_avg && !avg_first) av[i] = avg_x[j];
+        if (!kNonneg) {
+          ll[i] = l[j];
+          uu[i] = u[j];
+        }
+      }
+#pragma unroll
+    for (int i = 0; i < RPT; ++i)
+      if (i < nvalid) {
+        const int j = j0 + i * stride;
+        const double s = acc[i][0];
+        kty_out[j] = s;
+        if (do_avg) avg_x[j] = avg_first ? xa[i] : av[i] + ratio * (xa[i] - av[i]);
+        const double v = xa[i] - tau * (cc[i] - s);  // solver.hpp:404-408
+        const double xn = kNonneg ? smax(v, 0.0) : clamp_box(v, ll[i], uu[i]);
+        xt[j] = xn;
+        const double d = xn - xa[i];
+        const double dd = d * d;
+        if (kSeq) seq_dx2[j] = dd;
+        red[0] += dd;
+        red[1] += isfinite(xn) ? 0.0 : 1.0;
+      }
   }
 };
 

@@ -52,10 +52,13 @@ __device__ double seq_sum_sq(const double* v, int n) {
 }
 
 // Outcome of the step decision (adaptive_step_cached, solver.hpp:436-466).
+constexpr int kHeadTab = 128;  // step factors staged at the primal head
+
 struct Decision {
   int mode;  // kPAccept / kPRetry / kPNone
   int cont;  // run another trial in this window
   double eta;  // step size of the next trial
+  double omega;
   double ratio;
   int first;
   int ix_cur, ix_trial, iy_cur, ikty_cur;
@@ -65,12 +68,14 @@ struct Decision {
 // The decision from the reduced trial terms, on the pre-decision state `s`.
 // `st` (may be null) receives the new state; `log` the accepted step.
 __device__ Decision step_decision(const DevState& s, const DevIter& it, double dy2, double inter,
-                                  double dx2, bool finite, DevState* st) {
+                                  double dx2, bool finite, double red_k, double gro_k,
+                                  DevState* st) {
   Decision d;
   const double omega = s.omega, eta = s.eta;
   d.cont = 0;
   d.mode = kPNone;
   d.eta = eta;
+  d.omega = omega;
   d.ratio = s.avg_ratio;
   d.first = s.avg_first;
   d.ix_cur = s.ix_cur, d.ix_trial = s.ix_trial, d.iy_cur = s.iy_cur, d.ikty_cur = s.ikty_cur;
@@ -90,8 +95,7 @@ __device__ Decision step_decision(const DevState& s, const DevIter& it, double d
   const double movement = omega * dx2 + dy2 / omega;  // solver.hpp:436
   const double ia = fabs(inter);
   const double eta_bar = ia > 0.0 ? movement / (2.0 * ia) : INFINITY;
-  const int64_t ti = s.total - s.table_base;
-  const double eta_next = smin(it.red_tab[ti] * eta_bar, it.gro_tab[ti] * eta);
+  const double eta_next = smin(red_k * eta_bar, gro_k * eta);
   d.eta = eta_next;
   if (eta <= eta_bar) {  // accept
     const double w = s.wsum + eta;  // WeightedAverage::add
@@ -169,7 +173,17 @@ __global__ void __launch_bounds__(kThreads, 4) dual_kernel(DevCsr K, DevIter it,
   prefetch_tile(t, K.rp, K.col, K.val);
   griddep_wait();  // x' and the state come from the previous primal kernel
   DevState* st = it.st;
-  if (!kSeq && blockIdx.x == 0 && threadIdx.x == 0) *it.snap = *st;
+  if (!kSeq && blockIdx.x == 0) {
+    if (threadIdx.x == 0) *it.snap = *st;
+    // the primal partials of x' (the decision's dx^2) are reduced here, off the
+    // critical path, so the decision at the primal head has one round trip
+    double pp[2];
+    sum_partials<2, 0>(it.p_part + size_t(st->trials_total & 1) * it.p_grid * 2, it.p_grid, pp);
+    if (threadIdx.x == 0) {
+      it.px_total[0] = pp[0];
+      it.px_total[1] = pp[1];
+    }
+  }
   // A failed or completed window parks the remaining (stream-engine) launches.
   if (st->failure || st->window_accepts >= st->window_target) {
     if (kSeq && blockIdx.x == 0 && threadIdx.x == 0) st->p_mode = kPNone;
@@ -207,7 +221,9 @@ __global__ void __launch_bounds__(kThreads, 4) dual_kernel(DevCsr K, DevIter it,
     inter += __ldcg(it.seq_inter + i);
   }
   const DevState pre = *st;
-  const Decision d = step_decision(pre, it, dy2, inter, dx2, dpart[2] == 0.0 && ppart[1] == 0.0, st);
+  const int64_t ti = pre.total - pre.table_base;
+  const Decision d = step_decision(pre, it, dy2, inter, dx2, dpart[2] == 0.0 && ppart[1] == 0.0,
+                                   it.red_tab[ti], it.gro_tab[ti], st);
   __threadfence();
   if (use_cond) cudaGraphSetConditional(cond, d.cont ? 1u : 0u);
 }
@@ -237,34 +253,80 @@ __global__ void __launch_bounds__(kThreads, 4) primal_kernel(DevCsr KT, DevIter 
     const DevState& s = *st;
     d.mode = mode_override >= 0 ? mode_override : s.p_mode;
     d.eta = s.eta;
+    d.omega = s.omega;
     d.ratio = s.avg_ratio;
     d.first = s.avg_first;
     d.ix_cur = s.ix_cur, d.ix_trial = s.ix_trial, d.iy_cur = s.iy_cur, d.ikty_cur = s.ikty_cur;
     d.trials = s.trials_total;
   } else {
-    const DevState& s = *it.snap;  // the state the dual kernel of this trial ran on
-    if (s.failure || s.window_accepts >= s.window_target) return;
-    double dp[3], pp[2];
+    // decision inputs, all issued as independent loads (one round trip): the
+    // state snapshot the dual kernel ran on, the window's step-factor table,
+    // the pre-reduced dx^2, and the dual partials
+    __shared__ DevState s_snap;
+    __shared__ double s_tab[2][kHeadTab];
+    __shared__ double s_px[2];
+    constexpr int kWords = int(sizeof(DevState) / sizeof(unsigned long long));
+    const int tid = threadIdx.x;
+    unsigned long long w = 0;
+    if (tid < kWords) w = __ldcg(reinterpret_cast<const unsigned long long*>(it.snap) + tid);
+    double tr = 0.0, tg = 0.0, px = 0.0;
+    if (tid < kHeadTab) {
+      tr = __ldcg(it.red_tab + tid);
+      tg = __ldcg(it.gro_tab + tid);
+    }
+    if (tid < 2) px = __ldcg(it.px_total + tid);
+    double dp[3];
     sum_partials<3, 0>(it.d_part, it.d_tiles, dp);
-    sum_partials<2, 0>(it.p_part + size_t(s.trials_total & 1) * it.p_grid * 2, it.p_grid, pp);
-    if (threadIdx.x == 0) {
-      const bool commit = bid == 0;
-      sd = step_decision(s, it, dp[0], dp[1], pp[0], dp[2] == 0.0 && pp[1] == 0.0,
-                         commit ? st : nullptr);
-      if (commit) {
-        __threadfence();
-        if (use_cond) cudaGraphSetConditional(cond, sd.cont ? 1u : 0u);
+    if (tid < kWords) reinterpret_cast<unsigned long long*>(&s_snap)[tid] = w;
+    if (tid < kHeadTab) {
+      s_tab[0][tid] = tr;
+      s_tab[1][tid] = tg;
+    }
+    if (tid < 2) s_px[tid] = px;
+    __syncthreads();
+    if (tid == 0) {
+      const DevState& s = s_snap;
+      if (s.failure || s.window_accepts >= s.window_target) {
+        sd.mode = kPNone;  // parked launch of a completed window (stream engine)
+      } else {
+        const bool commit = bid == 0;
+        const int64_t ti = s.total - s.table_base;
+        const double rk = ti < kHeadTab ? s_tab[0][ti] : it.red_tab[ti];
+        const double gk = ti < kHeadTab ? s_tab[1][ti] : it.gro_tab[ti];
+        sd = step_decision(s, it, dp[0], dp[1], s_px[0], dp[2] == 0.0 && s_px[1] == 0.0, rk, gk,
+                           commit ? st : nullptr);
+        if (commit) {
+          __threadfence();
+          if (use_cond) cudaGraphSetConditional(cond, sd.cont ? 1u : 0u);
+        }
       }
     }
     __syncthreads();
     d = sd;
+    if (d.mode == kPNone) return;
   }
   if (d.mode == kPNone) return;  // keep the partials of the last real trial
   double red[2] = {0.0, 0.0};
-  const double tau = d.eta / st->omega;  // tau = eta / omega, solver.hpp:401
+  const double tau = d.eta / d.omega;  // tau = eta / omega, solver.hpp:401
   if (d.mode == kPAccept || d.mode == kPRestart) {
     const bool acc = d.mode == kPAccept;
     if (bid < KT.ntiles) {
+      {
+        // the epilogue's contiguous operands of this tile's columns -> L2 while
+        // the matrix and the gathers are in flight
+        const Tile tt = KT.tiles[bid];
+        const int j0 = tt.kind == kTileChunk ? tt.row0 : tt.row0;
+        const int j1 = tt.kind == kTileChunk ? tt.row0 + 1 : tt.row1;
+        for (int j = (j0 & ~15) + 16 * int(threadIdx.x); j < j1; j += 16 * kThreads) {
+          prefetch_l2(it.x[d.ix_cur] + j);
+          prefetch_l2(it.c + j);
+          if (acc) prefetch_l2(it.avg_x + j);
+          if (!kNonneg) {
+            prefetch_l2(it.l + j);
+            prefetch_l2(it.u + j);
+          }
+        }
+      }
       PrimalEpi<kSeq, kNonneg> epi;
       epi.yg = it.y[d.iy_cur];
       epi.xc = it.x[d.ix_cur];
@@ -526,6 +588,7 @@ struct Ev2Epi : EpiBase<Ev2Epi<kSeq>> {
   double* __restrict__ lam;
   double* __restrict__ seq_d;
   int n, m1;
+  int lam_slot;  // slot whose reduced costs are stored (-1: none; parity mode: all)
   __device__ __forceinline__ void gather(int r, double (&g)[4]) const { load4(Y4 + size_t(r) * 4, g); }
   __device__ __forceinline__ void add(double (&a)[8], const double (&p)[4], int col) const {
     if (col < m1) {
@@ -544,7 +607,7 @@ struct Ev2Epi : EpiBase<Ev2Epi<kSeq>> {
     for (int s = 0; s < 2; ++s) {
       const double slack = (cj + -1.0 * a[s]) + -1.0 * a[4 + s];
       const double lm = reduced_cost(slack, lj, uj);
-      lam[size_t(s) * n + j] = lm;
+      if (kSeq || s == lam_slot) lam[size_t(s) * n + j] = lm;
       const double dres = slack + -1.0 * lm;
       if (kSeq) seq_d[size_t(s) * n + j] = dres;
       red[s * 3 + 0] += dres * dres;
@@ -555,7 +618,7 @@ struct Ev2Epi : EpiBase<Ev2Epi<kSeq>> {
     for (int s = 2; s < 4; ++s) {
       const double kty = a[s] + 1.0 * a[4 + s];
       const double lm = reduced_cost(-kty, lj, uj);
-      lam[size_t(s) * n + j] = lm;
+      if (kSeq || s == lam_slot) lam[size_t(s) * n + j] = lm;
       const double viol = kty + 1.0 * lm;
       if (kSeq) seq_d[size_t(s) * n + j] = viol;
       const int o = 6 + (s - 2) * 4;
@@ -578,23 +641,26 @@ __global__ void __launch_bounds__(kThreads) eval_rows_kernel(DevCsr K, DevEval e
   double red[14];
 #pragma unroll
   for (int i = 0; i < 14; ++i) red[i] = i < 12 ? 0.0 : -INFINITY;
-  const Tile t = K.tiles[blockIdx.x];
-  run_tile<Ev1Epi<kSeq>, kSeq>(t, K.rp, K.col, K.val_orig, epi, red, K.chunk_part, K.chunk_ctr, smem);
+  // each CTA walks several tiles, so the final reduction sums one partial per CTA
+  for (int ti = blockIdx.x; ti < K.ntiles; ti += gridDim.x)
+    run_tile<Ev1Epi<kSeq>, kSeq>(K.tiles[ti], K.rp, K.col, K.val_orig, epi, red, K.chunk_part,
+                                 K.chunk_ctr, smem);
   store_partial<12, 2>(red, ev.part1, blockIdx.x);
 }
 
 template <bool kSeq>
-__global__ void __launch_bounds__(kThreads) eval_cols_kernel(DevCsr KT, DevEval ev, int n, int m1) {
+__global__ void __launch_bounds__(kThreads) eval_cols_kernel(DevCsr KT, DevEval ev, int n, int m1,
+                                                             int lam_slot) {
   extern __shared__ __align__(16) unsigned char smem[];
   Ev2Epi<kSeq> epi;
   epi.Y4 = ev.Y4, epi.X4 = ev.X4, epi.c = ev.c, epi.l = ev.l, epi.u = ev.u, epi.lam = ev.lam;
-  epi.seq_d = ev.seq_d, epi.n = n, epi.m1 = m1;
+  epi.seq_d = ev.seq_d, epi.n = n, epi.m1 = m1, epi.lam_slot = lam_slot;
   double red[18];
 #pragma unroll
   for (int i = 0; i < 18; ++i) red[i] = i < 14 ? 0.0 : -INFINITY;
-  const Tile t = KT.tiles[blockIdx.x];
-  run_tile<Ev2Epi<kSeq>, kSeq>(t, KT.rp, KT.col, KT.val_orig, epi, red, KT.chunk_part, KT.chunk_ctr,
-                              smem);
+  for (int ti = blockIdx.x; ti < KT.ntiles; ti += gridDim.x)
+    run_tile<Ev2Epi<kSeq>, kSeq>(KT.tiles[ti], KT.rp, KT.col, KT.val_orig, epi, red, KT.chunk_part,
+                                 KT.chunk_ctr, smem);
   store_partial<14, 4>(red, ev.part2, blockIdx.x);
 }
 
@@ -1080,6 +1146,8 @@ void launch_restart_copy(const DevIter& it, int from_avg, cudaStream_t s) {
   PDLP_CUDA(cudaGetLastError());
 }
 
+int eval_grid(int ntiles) { return ntiles; }  // one tile per CTA: short latency chains
+
 void launch_eval(const DevCsr& k, const DevCsr& kt, const DevIter& it, const DevEval& ev, bool seq,
                  cudaStream_t s) {
   const int span = kThreads * kEv0Items;
@@ -1088,16 +1156,25 @@ void launch_eval(const DevCsr& k, const DevCsr& kt, const DevIter& it, const Dev
   PDLP_CUDA(cudaGetLastError());
   const size_t sm1 = stream_smem_bytes<Ev1Epi<false>>();
   const size_t sm2 = stream_smem_bytes<Ev2Epi<false>>();
+  const int g1 = eval_grid(k.ntiles), g2 = eval_grid(kt.ntiles);
   if (seq) {
-    if (k.ntiles) eval_rows_kernel<true><<<k.ntiles, kThreads, sm1, s>>>(k, ev, it.m, it.m1);
-    if (kt.ntiles) eval_cols_kernel<true><<<kt.ntiles, kThreads, sm2, s>>>(kt, ev, it.n, it.m1);
-    eval_final_kernel<true><<<1, kThreads, 0, s>>>(ev, k.ntiles, kt.ntiles, it.n, it.m, it.m1);
+    eval_rows_kernel<true><<<g1, kThreads, sm1, s>>>(k, ev, it.m, it.m1);
+    eval_cols_kernel<true><<<g2, kThreads, sm2, s>>>(kt, ev, it.n, it.m1, -1);
+    eval_final_kernel<true><<<1, kThreads, 0, s>>>(ev, g1, g2, it.n, it.m, it.m1);
     eval_seq_displacement_kernel<<<1, 32, 0, s>>>(it, ev.out);
   } else {
-    if (k.ntiles) eval_rows_kernel<false><<<k.ntiles, kThreads, sm1, s>>>(k, ev, it.m, it.m1);
-    if (kt.ntiles) eval_cols_kernel<false><<<kt.ntiles, kThreads, sm2, s>>>(kt, ev, it.n, it.m1);
-    eval_final_kernel<false><<<1, kThreads, 0, s>>>(ev, k.ntiles, kt.ntiles, it.n, it.m, it.m1);
+    eval_rows_kernel<false><<<g1, kThreads, sm1, s>>>(k, ev, it.m, it.m1);
+    eval_cols_kernel<false><<<g2, kThreads, sm2, s>>>(kt, ev, it.n, it.m1, -1);
+    eval_final_kernel<false><<<1, kThreads, 0, s>>>(ev, g1, g2, it.n, it.m, it.m1);
   }
+  PDLP_CUDA(cudaGetLastError());
+}
+
+void launch_eval_lambda(const DevCsr& kt, const DevIter& it, const DevEval& ev, bool seq, int slot,
+                        cudaStream_t s) {
+  if (seq) return;  // parity mode stores every slot's reduced costs on each evaluation
+  const size_t sm2 = stream_smem_bytes<Ev2Epi<false>>();
+  eval_cols_kernel<false><<<eval_grid(kt.ntiles), kThreads, sm2, s>>>(kt, ev, it.n, it.m1, slot);
   PDLP_CUDA(cudaGetLastError());
 }
 

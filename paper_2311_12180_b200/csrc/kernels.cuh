@@ -58,6 +58,10 @@ void launch_restart_copy(const DevIter& it, int from_avg, cudaStream_t s);
 void launch_eval(const DevCsr& k, const DevCsr& kt, const DevIter& it, const DevEval& ev,
                  bool seq, cudaStream_t s);
 int eval_grid0(int n, int m);
+int eval_grid(int ntiles);
+// Reduced costs of one evaluated point (slot 0..3) into lam[slot] (finish only).
+void launch_eval_lambda(const DevCsr& kt, const DevIter& it, const DevEval& ev, bool seq, int slot,
+                        cudaStream_t s);
 void launch_reduced_of_objective(const double* c, const double* l, const double* u, int n,
                                  double* lam, cudaStream_t s);
 

@@ -376,8 +376,10 @@ void Solver::allocate_iteration() {
   seq_inter_.alloc(seq ? m_ : 1);
   seq_dx2_.alloc(seq ? n_ : 1);
   tab_cap_ = int(std::min<int64_t>(params_.evaluation_frequency, 4096));
-  red_tab_.alloc(tab_cap_);
-  gro_tab_.alloc(tab_cap_);
+  red_tab_.alloc(std::max(tab_cap_, 128));  // the primal head stages 128 entries
+  gro_tab_.alloc(std::max(tab_cap_, 128));
+  red_tab_.zero(s);
+  gro_tab_.zero(s);
   step_log_dev_.alloc(tab_cap_);
   state_dev_.alloc(1);
   snap_dev_.alloc(1);
@@ -454,8 +456,8 @@ void Solver::allocate_iteration() {
   scratch_n_.alloc(n_);
   const int grid0 = eval_grid0(int(n_), int(m_));
   part0_.alloc(size_t(std::max(1, grid0)) * 4);
-  part1_.alloc(size_t(k_ev_.csr.ntiles) * 14);
-  part2_.alloc(size_t(kt_ev_.csr.ntiles) * 18);
+  part1_.alloc(size_t(eval_grid(k_ev_.csr.ntiles)) * 14);
+  part2_.alloc(size_t(eval_grid(kt_ev_.csr.ntiles)) * 18);
   seq_r_.alloc(seq ? size_t(m_) * 4 : 1);
   seq_d_.alloc(seq ? size_t(n_) * 4 : 1);
   eval_dev_.alloc(1);
@@ -551,6 +553,7 @@ void Solver::iterate_begin(int32_t* status) {
   window_seconds_ = 0.0;
   PDLP_CUDA(cudaEventRecord(ev_begin_, stream_));
   upload_state();
+  eval_fresh_ = false;
   launch_zero_iterate(it_, stream_);  // z = 0, Kx = K 0 = 0, K'y = 0 (solver.hpp:764-769)
   ++launches_;
   // initial evaluation on the unscaled zero point (solver.hpp:784-792)
@@ -628,6 +631,7 @@ void Solver::run_window(int target) {
   PDLP_CUDA(cudaMemcpyAsync(gro_tab_.get(), gro, target * sizeof(double), cudaMemcpyHostToDevice,
                             stream_));
   upload_state();
+  eval_fresh_ = false;
   PDLP_CUDA(cudaEventRecord(ev_w0_, stream_));
   if (engine_ == PDLP_ENGINE_PERSISTENT) {
     WinBufs wb = wb_;
@@ -635,15 +639,11 @@ void Solver::run_window(int target) {
                               : it_.p_part + size_t(st.trials_total & 1) * it_.p_grid * 2;
     wb.p_src_count = p_from_window_ ? win_grid_ : it_.p_grid;
     launch_window(k_win_.csr, kt_win_.csr, it_, wb, win_grid_, stream_);
-    PDLP_CUDA(cudaEventRecord(ev_w1_, stream_));
-    download_state();
     p_from_window_ = true;
     launches_ += 1;
   } else if (engine_ == PDLP_ENGINE_GRAPH) {
     if (!graph_exec_) capture_window_graph();
     PDLP_CUDA(cudaGraphLaunch(graph_exec_, stream_));
-    PDLP_CUDA(cudaEventRecord(ev_w1_, stream_));
-    download_state();
   } else {
     int remaining = target;
     while (true) {
@@ -651,28 +651,39 @@ void Solver::run_window(int target) {
         launch_dual(K_, it_, parity(), 0, 0, stream_);
         launch_primal(KT_, it_, parity(), -1, stream_);
       }
-      PDLP_CUDA(cudaEventRecord(ev_w1_, stream_));
       download_state();
       if (st.failure || st.window_accepts >= target) break;
       remaining = target - st.window_accepts;
     }
   }
+  PDLP_CUDA(cudaEventRecord(ev_w1_, stream_));
+  // the evaluation block is enqueued behind the window (it reads the device
+  // state), so one host round trip per window brings back state, scalars, log
+  launch_eval(k_ev_.csr, kt_ev_.csr, it_, ev_, parity(), stream_);
+  launches_ += parity() ? 5 : 4;
+  ++evaluations_;
+  PDLP_CUDA(cudaMemcpyAsync(hs_.get(), state_dev_.get(), sizeof(DevState), cudaMemcpyDeviceToHost,
+                            stream_));
+  PDLP_CUDA(cudaMemcpyAsync(he_.get(), eval_dev_.get(), sizeof(EvalOut), cudaMemcpyDeviceToHost,
+                            stream_));
+  if (st.record_log)
+    PDLP_CUDA(cudaMemcpyAsync(log_host_.get(), step_log_dev_.get(),
+                              size_t(target) * sizeof(pdlp_step_log_entry), cudaMemcpyDeviceToHost,
+                              stream_));
+  PDLP_CUDA(cudaStreamSynchronize(stream_));
+  eval_fresh_ = true;
   {
     float ms = 0.f;
     PDLP_CUDA(cudaEventElapsedTime(&ms, ev_w0_, ev_w1_));
     window_seconds_ += 1e-3 * double(ms);
   }
   if (engine_ != PDLP_ENGINE_PERSISTENT) launches_ += 2 * (st.trials_total - trials_before);
-  if (st.record_log && st.window_accepts > 0) {
-    PDLP_CUDA(cudaMemcpyAsync(log_host_.get(), step_log_dev_.get(),
-                              st.window_accepts * sizeof(pdlp_step_log_entry),
-                              cudaMemcpyDeviceToHost, stream_));
-    PDLP_CUDA(cudaStreamSynchronize(stream_));
+  if (st.record_log && st.window_accepts > 0)
     step_log_.insert(step_log_.end(), log_host_.get(), log_host_.get() + st.window_accepts);
-  }
 }
 
 void Solver::evaluate() {
+  if (eval_fresh_) return;  // nothing changed since the window's own evaluation
   upload_state();
   launch_eval(k_ev_.csr, kt_ev_.csr, it_, ev_, parity(), stream_);
   launches_ += parity() ? 5 : 4;
@@ -680,6 +691,7 @@ void Solver::evaluate() {
   PDLP_CUDA(cudaMemcpyAsync(he_.get(), eval_dev_.get(), sizeof(EvalOut), cudaMemcpyDeviceToHost,
                             stream_));
   PDLP_CUDA(cudaStreamSynchronize(stream_));
+  eval_fresh_ = true;
 }
 
 KktHost Solver::kkt(int slot) const {
@@ -773,6 +785,7 @@ void Solver::evaluation_block() {
   launch_spmv(K_, false, it_.x[st.ix_cur], it_.kx[st.ikx_cur], parity(), stream_);
   launch_primal(KT_, it_, parity(), kPRestart, stream_);
   launches_ += 3;
+  eval_fresh_ = false;
   p_from_window_ = false;
   ev.omega_after = st.omega;
   restart_log_.push_back(ev);
@@ -805,6 +818,7 @@ void Solver::finish(int status, int slot_x, int slot_y, int slot_lam, const KktH
                                 sizeof(double), m_, cudaMemcpyDeviceToHost, s));
   if (n_) {
     if (slot_lam >= 0) {
+      launch_eval_lambda(kt_ev_.csr, it_, ev_, parity(), slot_lam, s);
       PDLP_CUDA(cudaMemcpyAsync(rlam_.data(), lam_.get() + size_t(slot_lam) * n_,
                                 n_ * sizeof(double), cudaMemcpyDeviceToHost, s));
     } else {

@@ -178,6 +178,7 @@ class Solver {
   int engine_ = PDLP_ENGINE_PERSISTENT;
   int win_grid_ = 0;
   bool p_from_window_ = false;
+  bool eval_fresh_ = false;  // EvalOut on the host matches the device state
   DevBuf<double> wd_part_, wp_part_;
   DevBuf<GridBar> bar_;
   WinBufs wb_{};

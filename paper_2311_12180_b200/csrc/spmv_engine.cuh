@@ -59,6 +59,15 @@ struct EpiBase {
                                             double (&red)[NR]) const {
     for (int i = 0; i < nr; ++i) static_cast<const D*>(this)->row_done(r0 + i, acc[i], red);
   }
+  // rows r0 + i * stride, i < nvalid (the STREAM tile's round-robin rows)
+  template <int RPT, int NA, int NR>
+  __device__ __forceinline__ void rows_strided(int r0, int stride, int nvalid,
+                                               const double (&acc)[RPT][NA],
+                                               double (&red)[NR]) const {
+#pragma unroll
+    for (int i = 0; i < RPT; ++i)
+      if (i < nvalid) static_cast<const D*>(this)->row_done(r0 + i * stride, acc[i], red);
+  }
 };
 
 // Loads in flight per lane: 2 quads (8 nnz) per batch for the scalar-gather kernels.
@@ -193,33 +202,30 @@ __device__ void run_tile(const Tile& t, const int* __restrict__ rp, const int* _
       }
     }
     __syncthreads();
-    // each thread owns groups of 4 consecutive rows and sums each row in index
-    // order from the staged products
-    constexpr int kGroups = Epi::kGeom.stream_rows / (4 * kThreads);
+    // rows are dealt round-robin (thread t: rows row0 + t + i * kThreads), so a
+    // warp reads neighbouring products from shared memory (no bank conflicts)
+    // and neighbouring epilogue operands from HBM (coalesced); each row is
+    // summed in index order
+    constexpr int RPT = Epi::kGeom.stream_rows / kThreads;
+    double acc[RPT][Epi::NA];
+    int nvalid = 0;
 #pragma unroll
-    for (int gi = 0; gi < kGroups; ++gi) {
-      const int r0 = t.row0 + 4 * (tid + gi * kThreads);
-      if (r0 >= t.row1) break;
-      const int nr = min(4, t.row1 - r0);
-      int bounds[5];
+    for (int i = 0; i < RPT; ++i) {
+      const int r = t.row0 + tid + i * kThreads;
 #pragma unroll
-      for (int i = 0; i < 5; ++i) bounds[i] = i <= nr ? rp[r0 + i] - t.k0 : 0;
-      double acc[4][Epi::NA];
+      for (int j = 0; j < Epi::NA; ++j) acc[i][j] = 0.0;
+      if (r < t.row1) {
+        nvalid = i + 1;
+        const int a = rp[r] - t.k0, b = rp[r + 1] - t.k0;
+        for (int s = a; s < b; ++s) {
+          double p[Epi::NP];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-#pragma unroll
-        for (int j = 0; j < Epi::NA; ++j) acc[i][j] = 0.0;
-        if (i < nr) {
-          for (int s = bounds[i]; s < bounds[i + 1]; ++s) {
-            double p[Epi::NP];
-#pragma unroll
-            for (int j = 0; j < Epi::NP; ++j) p[j] = sprod[size_t(s) * Epi::NP + j];
-            epi.add(acc[i], p, Epi::kNeedCol ? scol[s] : 0);
-          }
+          for (int j = 0; j < Epi::NP; ++j) p[j] = sprod[size_t(s) * Epi::NP + j];
+          epi.add(acc[i], p, Epi::kNeedCol ? scol[s] : 0);
         }
       }
-      epi.rows_done(r0, nr, acc, red);
     }
+    epi.template rows_strided<RPT>(t.row0 + tid, kThreads, nvalid, acc, red);
     __syncthreads();
   } else if (t.kind == kTileWarp) {
     // G lanes per row (t.part in {8,...,256}, ~8 nnz per lane: one batch of

@@ -142,21 +142,20 @@ __device__ __forceinline__ void staged_tile(const Tile& t, const Stage& sg, doub
       }
     }
     __syncthreads();
-    const int r0 = t.row0 + 4 * tid;
-    if (r0 < t.row1) {
-      const int nr = min(4, t.row1 - r0);
-      int bounds[5];
+    constexpr int RPT = kWinGeom.stream_rows / kThreads;  // round-robin rows (no bank conflicts)
+    double acc[RPT][1];
+    int nvalid = 0;
 #pragma unroll
-      for (int i = 0; i < 5; ++i) bounds[i] = i <= nr ? sg.rp[r0 + i - r0a] - t.k0 : 0;
-      double acc[4][1];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        acc[i][0] = 0.0;
-        if (i < nr)
-          for (int s = bounds[i]; s < bounds[i + 1]; ++s) acc[i][0] += prod[s];
+    for (int i = 0; i < RPT; ++i) {
+      const int r = t.row0 + tid + i * kThreads;
+      acc[i][0] = 0.0;
+      if (r < t.row1) {
+        nvalid = i + 1;
+        const int a = sg.rp[r - r0a] - t.k0, b = sg.rp[r + 1 - r0a] - t.k0;
+        for (int s2 = a; s2 < b; ++s2) acc[i][0] += prod[s2];
       }
-      epi.rows_done(r0, nr, acc, red);
     }
+    epi.template rows_strided<RPT>(t.row0 + tid, kThreads, nvalid, acc, red);
   } else if (t.kind == kTileWarp) {
     const int r0a = t.row0 & ~3;
     const int G = t.part;
