@@ -44,6 +44,45 @@ void validate_params(const pdlp_params& p) {  // SolverParams::validate, solver.
   if (p.mode != PDLP_MODE_FAST && p.mode != PDLP_MODE_PARITY) invalid("params: unknown mode");
 }
 
+// GeneralFormLp::validate (lp_model.hpp:45-72), then SolverParams::validate;
+// runs before any CUDA call so invalid input is PDLP_EINVAL even without a GPU.
+void validate_input(const pdlp_lp& lp, const pdlp_params& params) {
+  const pdlp_csr& G = lp.inequality_matrix;
+  const pdlp_csr& A = lp.equality_matrix;
+  const int64_t n = lp.num_variables;
+  if (n < 0 || G.num_rows < 0 || A.num_rows < 0 || G.nnz < 0 || A.nnz < 0)
+    invalid("lp: negative dimension");
+  if (G.num_cols != n || A.num_cols != n) invalid("lp: constraint matrices must have n columns");
+  const int64_t m1 = G.num_rows, m2 = A.num_rows, m = m1 + m2, nnz = G.nnz + A.nnz;
+  auto need = [](const void* p, int64_t len, const char* what) {
+    if (len > 0 && !p) invalid(std::string("lp: missing ") + what);
+  };
+  need(lp.objective, n, "objective");
+  need(lp.lower, n, "lower bounds");
+  need(lp.upper, n, "upper bounds");
+  need(lp.inequality_rhs, m1, "inequality rhs");
+  need(lp.equality_rhs, m2, "equality rhs");
+  for (const pdlp_csr* c : {&G, &A}) {
+    need(c->values, c->nnz, "matrix values");
+    if (c->nnz > 0 && !c->col_indices && !c->col_indices32) invalid("lp: missing column indices");
+    if (c->num_rows > 0 && !c->row_offsets) invalid("lp: missing row offsets");
+    if (c->row_offsets && (c->row_offsets[0] != 0 || c->row_offsets[c->num_rows] != c->nnz))
+      invalid("csr: row_offsets must start at 0 and end at nnz");
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    const double l = lp.lower[i], u = lp.upper[i];
+    if (std::isnan(l) || std::isnan(u)) invalid("lp: NaN bound on variable " + std::to_string(i));
+    if (l > u || l == INFINITY || u == -INFINITY)
+      invalid("lp: empty bound interval on variable " + std::to_string(i));
+  }
+  for (int64_t i = 0; i < n; ++i)
+    if (std::isnan(lp.objective[i])) invalid("lp: NaN objective entry");
+  validate_params(params);
+  const int64_t lim = int64_t(std::numeric_limits<int32_t>::max()) - 1024;
+  if (n > lim || m > lim || nnz > lim)
+    throw std::runtime_error("instance exceeds the 32-bit index layout of one device (shard it)");
+}
+
 double seq_norm2(const std::vector<double>& v) {
   double s = 0.0;
   for (double x : v) s += x * x;
@@ -63,6 +102,7 @@ double KktHost::weighted(double omega) const {  // KktResiduals::weighted
 
 Solver::Solver(const pdlp_lp& lp, const pdlp_params& params) : params_(params) {
   const auto t = std::chrono::steady_clock::now();
+  validate_input(lp, params);
   PDLP_CUDA(cudaSetDevice(params.device));
   PDLP_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   setup(lp);
@@ -81,44 +121,14 @@ Solver::~Solver() {
 }
 
 void Solver::setup(const pdlp_lp& lp) {
-  // ---- GeneralFormLp::validate (lp_model.hpp:45-72), then params ----
+  // validated by validate_input() before any device work
   const pdlp_csr& G = lp.inequality_matrix;
   const pdlp_csr& A = lp.equality_matrix;
   n_ = lp.num_variables;
-  if (n_ < 0 || G.num_rows < 0 || A.num_rows < 0 || G.nnz < 0 || A.nnz < 0)
-    invalid("lp: negative dimension");
-  if (G.num_cols != n_ || A.num_cols != n_) invalid("lp: constraint matrices must have n columns");
   m1_ = G.num_rows;
   m2_ = A.num_rows;
   m_ = m1_ + m2_;
   nnz_ = G.nnz + A.nnz;
-  auto need = [](const void* p, int64_t len, const char* what) {
-    if (len > 0 && !p) invalid(std::string("lp: missing ") + what);
-  };
-  need(lp.objective, n_, "objective");
-  need(lp.lower, n_, "lower bounds");
-  need(lp.upper, n_, "upper bounds");
-  need(lp.inequality_rhs, m1_, "inequality rhs");
-  need(lp.equality_rhs, m2_, "equality rhs");
-  for (const pdlp_csr* c : {&G, &A}) {
-    need(c->values, c->nnz, "matrix values");
-    if (c->nnz > 0 && !c->col_indices && !c->col_indices32) invalid("lp: missing column indices");
-    if (c->num_rows > 0 && !c->row_offsets) invalid("lp: missing row offsets");
-    if (c->row_offsets && (c->row_offsets[0] != 0 || c->row_offsets[c->num_rows] != c->nnz))
-      invalid("csr: row_offsets must start at 0 and end at nnz");
-  }
-  for (int64_t i = 0; i < n_; ++i) {
-    const double l = lp.lower[i], u = lp.upper[i];
-    if (std::isnan(l) || std::isnan(u)) invalid("lp: NaN bound on variable " + std::to_string(i));
-    if (l > u || l == INFINITY || u == -INFINITY)
-      invalid("lp: empty bound interval on variable " + std::to_string(i));
-  }
-  for (int64_t i = 0; i < n_; ++i)
-    if (std::isnan(lp.objective[i])) invalid("lp: NaN objective entry");
-  validate_params(params_);
-  const int64_t lim = int64_t(std::numeric_limits<int32_t>::max()) - 1024;
-  if (n_ > lim || m_ > lim || nnz_ > lim)
-    throw std::runtime_error("instance exceeds the 32-bit index layout of one device (shard it)");
 
   objective_constant_ = lp.objective_constant;
   c_.assign(lp.objective, lp.objective + n_);
