@@ -13,6 +13,9 @@
  *   pdlp_get_scaling              <- make_scaling(vstack(G,A), ...) (scaling.hpp:117-132)
  *   pdlp_iterate_begin/run/get    <- SolveLoop::run's loop body, exposed for iterate parity
  *                                    (solver.hpp:759-841; detail::adaptive_step_cached :381-467)
+ *   pdlp_read_mps / pdlp_parse_mps <- read_mps_file / parse_mps + to_general_form
+ *                                    (mps_io.hpp:163-585), host C++ inside the library
+ *   pdlp_write_solution           <- write_solution (solution_io.hpp:70-95)
  *
  * Conventions (mirroring the reference):
  *   - plain pointers and sizes, no C++/torch types; caller-owned inputs are
@@ -65,6 +68,9 @@ enum {
 
 /* ---- ScalingMode (scaling.hpp:16) ------------------------------------ */
 enum { PDLP_SCALING_NONE = 0, PDLP_SCALING_RUIZ = 1, PDLP_SCALING_RUIZ_PC = 2 };
+
+/* ---- MpsFormat (mps_io.hpp:40) --------------------------------------- */
+enum { PDLP_MPS_FIXED = 0, PDLP_MPS_FREE = 1, PDLP_MPS_AUTO = 2 };
 
 /* ---- execution modes (B200 extension) -------------------------------- */
 enum {
@@ -264,6 +270,31 @@ int pdlp_time_kernel(pdlp_handle* h, int32_t which, int32_t reps, double* avg_ms
 
 /* Problem sizes after create: {n, m, m1, nnz}. */
 int pdlp_get_sizes(pdlp_handle* h, int64_t* sizes);
+
+/* ---- LP files (host I/O; no device work) ----------------------------- */
+
+/* An LP read from MPS text, owning its arrays (64-bit indices). */
+typedef struct pdlp_lp_file pdlp_lp_file;
+
+/* read_mps_file (mps_io.hpp:582-585): format PDLP_MPS_*; a path ending in
+ * ".gz" is inflated. Parse errors return PDLP_ERUNTIME with
+ * "mps parse error at line N: ..." (MpsParseError, mps_io.hpp:26-36); crossing
+ * bounds return PDLP_EINVAL (mps_io.hpp:536-546). */
+int pdlp_read_mps(const char* path, int32_t format, pdlp_lp_file** out);
+/* parse_mps + to_general_form (mps_io.hpp:163-554) on in-memory text. */
+int pdlp_parse_mps(const char* text, int64_t length, int32_t format, pdlp_lp_file** out);
+/* View of the GeneralFormLp (valid until pdlp_lp_file_free). */
+const pdlp_lp* pdlp_lp_file_lp(const pdlp_lp_file* f);
+/* NAME record and column names (index < num_variables). */
+const char* pdlp_lp_file_name(const pdlp_lp_file* f);
+const char* pdlp_lp_file_column_name(const pdlp_lp_file* f, int64_t index);
+void pdlp_lp_file_free(pdlp_lp_file* f);
+
+/* write_solution (solution_io.hpp:70-95): "format_version 1" key-value file with
+ * status, objectives, relative gap, residual norms, iterations and
+ * solve_seconds from *info; x (n) / y (m) blocks are written when non-NULL. */
+int pdlp_write_solution(const char* path, const pdlp_result_info* info, const double* x,
+                        int64_t n, const double* y, int64_t m);
 
 /* Thread-local message of the last failing call (valid until the next call). */
 const char* pdlp_last_error(void);

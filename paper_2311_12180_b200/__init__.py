@@ -15,7 +15,7 @@ from .lp import (
     SolverParams,
     SolveStatus,
 )
-from .api import PdlpError, Solver, load_library, solve
+from .api import PdlpError, Solver, load_library, parse_mps, read_mps, solve, write_solution
 
 __all__ = [
     "CsrMatrix",
@@ -33,4 +33,7 @@ __all__ = [
     "Solver",
     "load_library",
     "solve",
+    "read_mps",
+    "parse_mps",
+    "write_solution",
 ]

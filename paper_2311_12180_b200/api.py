@@ -60,6 +60,14 @@ def load_library(build_if_missing: bool = True) -> C.CDLL:
         "pdlp_time_kernel": (C.c_int, [H, C.c_int32, C.c_int32, dp, dp]),
         "pdlp_get_sizes": (C.c_int, [H, i64p]),
         "pdlp_last_error": (C.c_char_p, []),
+        "pdlp_read_mps": (C.c_int, [C.c_char_p, C.c_int32, C.POINTER(H)]),
+        "pdlp_parse_mps": (C.c_int, [C.c_char_p, C.c_int64, C.c_int32, C.POINTER(H)]),
+        "pdlp_lp_file_lp": (C.POINTER(abi.PdlpLp), [H]),
+        "pdlp_lp_file_name": (C.c_char_p, [H]),
+        "pdlp_lp_file_column_name": (C.c_char_p, [H, C.c_int64]),
+        "pdlp_lp_file_free": (None, [H]),
+        "pdlp_write_solution": (C.c_int, [C.c_char_p, C.POINTER(abi.PdlpResultInfo), dp, C.c_int64, dp,
+                                          C.c_int64]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -183,6 +191,72 @@ class Solver:
         return ms.value, by.value
 
 
+MPS_FIXED, MPS_FREE, MPS_AUTO = 0, 1, 2
+
+
+def _lp_from_file(lib, h) -> GeneralFormLp:
+    from .lp import CsrMatrix
+
+    v = lib.pdlp_lp_file_lp(h).contents
+
+    def csr(c):
+        rows, nnz = int(c.num_rows), int(c.nnz)
+        off = np.ctypeslib.as_array(c.row_offsets, (rows + 1,)).copy()
+        col = np.ctypeslib.as_array(c.col_indices, (nnz,)).copy() if nnz else np.zeros(0, np.int64)
+        val = np.ctypeslib.as_array(c.values, (nnz,)).copy() if nnz else np.zeros(0)
+        return CsrMatrix(rows, int(c.num_cols), off, col, val)
+
+    n = int(v.num_variables)
+    m1, m2 = int(v.inequality_matrix.num_rows), int(v.equality_matrix.num_rows)
+
+    def vec(p, k):
+        return np.ctypeslib.as_array(p, (k,)).copy() if k else np.zeros(0)
+
+    return GeneralFormLp(csr(v.inequality_matrix), csr(v.equality_matrix), vec(v.objective, n),
+                         vec(v.inequality_rhs, m1), vec(v.equality_rhs, m2), vec(v.lower, n), vec(v.upper, n),
+                         float(v.objective_constant))
+
+
+def read_mps(path, fmt: int = MPS_AUTO) -> GeneralFormLp:
+    """read_mps_file (mps_io.hpp:582-585), host C++ in libpdlp_b200.so. Parse
+    errors raise PdlpError naming the line; crossing bounds raise ValueError."""
+    lib = load_library()
+    h = C.c_void_p()
+    _check(lib.pdlp_read_mps(str(path).encode(), fmt, C.byref(h)))
+    try:
+        return _lp_from_file(lib, h)
+    finally:
+        lib.pdlp_lp_file_free(h)
+
+
+def parse_mps(text: str, fmt: int = MPS_AUTO) -> GeneralFormLp:
+    """parse_mps + to_general_form (mps_io.hpp:163-554) on in-memory text."""
+    lib = load_library()
+    b = text.encode()
+    h = C.c_void_p()
+    _check(lib.pdlp_parse_mps(b, len(b), fmt, C.byref(h)))
+    try:
+        return _lp_from_file(lib, h)
+    finally:
+        lib.pdlp_lp_file_free(h)
+
+
+def write_solution(result: SolveResult, path, include_vectors: bool = False) -> None:
+    """write_solution (solution_io.hpp:70-95)."""
+    lib = load_library()
+    info = abi.PdlpResultInfo()
+    info.status = int(result.status)
+    for k in ("primal_objective", "dual_objective", "relative_gap", "primal_residual_norm",
+              "dual_residual_norm"):
+        setattr(info, k, float(result.info[k]))
+    info.iterations = int(result.iterations)
+    info.solve_seconds = float(result.solve_seconds)
+    x = np.ascontiguousarray(result.point.primal, dtype=np.float64)
+    y = np.ascontiguousarray(result.point.dual, dtype=np.float64)
+    _check(lib.pdlp_write_solution(str(path).encode(), C.byref(info), abi.dptr(x) if include_vectors else None,
+                                   x.size, abi.dptr(y) if include_vectors else None, y.size))
+
+
 def solve(lp: GeneralFormLp, params: SolverParams | None = None) -> SolveResult:
     """pdhglp::solve (solver.hpp:935-940) on the GPU."""
     lp.validate()
@@ -191,4 +265,5 @@ def solve(lp: GeneralFormLp, params: SolverParams | None = None) -> SolveResult:
         return s.solve()
 
 
-__all__ = ["Solver", "solve", "load_library", "default_params", "PdlpError", "library_path"]
+__all__ = ["Solver", "solve", "load_library", "default_params", "PdlpError", "library_path", "read_mps",
+           "parse_mps", "write_solution", "MPS_FIXED", "MPS_FREE", "MPS_AUTO"]

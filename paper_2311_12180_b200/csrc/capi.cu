@@ -48,6 +48,10 @@ int null_handle() {
 
 }  // namespace
 
+namespace pdlp {
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace pdlp
+
 extern "C" {
 
 int pdlp_abi_version(void) { return PDLP_ABI_VERSION; }
