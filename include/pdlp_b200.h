@@ -152,7 +152,18 @@ typedef struct {
   int32_t use_cuda_graph;      /* 1: replay each evaluation window as a CUDA graph */
   int32_t l2_persist;          /* 1: pin the gathered iterate in L2 (access-policy window) */
   int32_t engine;              /* PDLP_ENGINE_*: how a window of iterations is driven */
-  int32_t reserved[6];
+  /* Row sharding: this handle is rank `rank` of `world_size`
+   * ranks (one per GPU), each running its contiguous share of the rows of K
+   * and of K^T; peers are linked with pdlp_shard_link_local (ranks in one
+   * process) or pdlp_shard_export / pdlp_shard_import (one process per GPU,
+   * CUDA IPC over NVLink). Fast mode only. */
+  int32_t world_size;          /* 1 */
+  int32_t rank;                /* 0 */
+  /* Tile breaks of a plan_world-way partition while running all rows on this
+   * handle (verification: a world_size = 1 run with plan_world = P matches a
+   * P-rank run bit for bit). 0 = world_size. */
+  int32_t plan_world;
+  int32_t reserved[3];
 } pdlp_params;
 
 /* ConvergenceInfo (solver.hpp:165-177) plus SolveResult scalars (:618-630). */
@@ -270,6 +281,26 @@ int pdlp_time_kernel(pdlp_handle* h, int32_t which, int32_t reps, double* avg_ms
 
 /* Problem sizes after create: {n, m, m1, nnz}. */
 int pdlp_get_sizes(pdlp_handle* h, int64_t* sizes);
+
+/* ---- row sharding (B200 extension) ---------------------------------- */
+
+/* Size of one rank's exported shard blob. */
+int64_t pdlp_shard_blob_size(void);
+/* Links the `world` ranks of one sharded solve that live in this process
+ * (handles in rank order; typically all on one device: the loopback transport
+ * used for verification). Their pdlp_solve calls must then run concurrently,
+ * one host thread per rank. */
+int pdlp_shard_link_local(pdlp_handle** handles, int32_t world);
+/* One process per GPU: every rank exports its blob (CUDA IPC handles of the
+ * buffers its peers write into), the caller all-gathers the blobs (e.g. over
+ * torch.distributed), then every rank imports all of them in rank order. */
+int pdlp_shard_export(pdlp_handle* h, void* blob, int64_t capacity);
+int pdlp_shard_import(pdlp_handle* h, const void* blobs, int32_t world);
+/* {world, rank, row0, row1, col0, col1, own K tiles, own K^T tiles, K tiles, K^T tiles} */
+int pdlp_shard_info(pdlp_handle* h, int64_t* out);
+/* Host-only: the row cuts (world + 1 each) of K = (G; A) and of K^T that a
+ * world-way sharded solve of `lp` uses. No device work. */
+int pdlp_plan_shards(const pdlp_lp* lp, int32_t world, int64_t* k_cuts, int64_t* kt_cuts);
 
 /* ---- LP files (host I/O; no device work) ----------------------------- */
 

@@ -15,7 +15,8 @@ from .lp import (
     SolverParams,
     SolveStatus,
 )
-from .api import PdlpError, Solver, load_library, parse_mps, read_mps, solve, write_solution
+from .api import (PdlpError, ShardGroup, Solver, load_library, parse_mps, plan_shards, read_mps, solve,
+                  solve_distributed, write_solution)
 
 __all__ = [
     "CsrMatrix",
@@ -36,4 +37,7 @@ __all__ = [
     "read_mps",
     "parse_mps",
     "write_solution",
+    "ShardGroup",
+    "plan_shards",
+    "solve_distributed",
 ]

@@ -83,7 +83,10 @@ class PdlpParams(C.Structure):
         ("use_cuda_graph", C.c_int32),
         ("l2_persist", C.c_int32),
         ("engine", C.c_int32),
-        ("reserved", C.c_int32 * 6),
+        ("world_size", C.c_int32),
+        ("rank", C.c_int32),
+        ("plan_world", C.c_int32),
+        ("reserved", C.c_int32 * 3),
     ]
 
 

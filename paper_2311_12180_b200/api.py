@@ -68,6 +68,12 @@ def load_library(build_if_missing: bool = True) -> C.CDLL:
         "pdlp_lp_file_free": (None, [H]),
         "pdlp_write_solution": (C.c_int, [C.c_char_p, C.POINTER(abi.PdlpResultInfo), dp, C.c_int64, dp,
                                           C.c_int64]),
+        "pdlp_shard_blob_size": (C.c_int64, []),
+        "pdlp_shard_link_local": (C.c_int, [C.POINTER(H), C.c_int32]),
+        "pdlp_shard_export": (C.c_int, [H, C.c_void_p, C.c_int64]),
+        "pdlp_shard_import": (C.c_int, [H, C.c_void_p, C.c_int32]),
+        "pdlp_shard_info": (C.c_int, [H, i64p]),
+        "pdlp_plan_shards": (C.c_int, [C.POINTER(abi.PdlpLp), C.c_int32, i64p, i64p]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -185,10 +191,110 @@ class Solver:
             "eta": sc[0], "eta_hat": sc[1], "omega": sc[2], "weight_sum": sc[3],
         }
 
+    # ---- row sharding ----
+    def shard_info(self) -> dict:
+        out = np.zeros(10, np.int64)
+        _check(self._lib.pdlp_shard_info(self._h, abi.i64ptr(out)))
+        keys = ("world", "rank", "row0", "row1", "col0", "col1", "k_tiles", "kt_tiles", "k_tiles_all",
+                "kt_tiles_all")
+        return {k: int(v) for k, v in zip(keys, out)}
+
+    def shard_export(self) -> bytes:
+        size = int(self._lib.pdlp_shard_blob_size())
+        buf = C.create_string_buffer(size)
+        _check(self._lib.pdlp_shard_export(self._h, buf, size))
+        return buf.raw
+
+    def shard_import(self, blobs: list[bytes]) -> None:
+        data = b"".join(blobs)
+        _check(self._lib.pdlp_shard_import(self._h, data, len(blobs)))
+
     def time_kernel(self, which: int, reps: int = 50) -> tuple[float, float]:
         ms, by = C.c_double(), C.c_double()
         _check(self._lib.pdlp_time_kernel(self._h, which, reps, C.byref(ms), C.byref(by)))
         return ms.value, by.value
+
+
+def plan_shards(lp: GeneralFormLp, world: int) -> tuple[np.ndarray, np.ndarray]:
+    """Row cuts (world + 1 each) of K = (G; A) and of K^T a world-way sharded
+    solve uses; host-only (no device)."""
+    lib = load_library()
+    kc, ktc = np.zeros(world + 1, np.int64), np.zeros(world + 1, np.int64)
+    lpa = lp.to_abi()
+    _check(lib.pdlp_plan_shards(C.byref(lpa), world, abi.i64ptr(kc), abi.i64ptr(ktc)))
+    return kc, ktc
+
+
+class ShardGroup:
+    """All ranks of one row-sharded solve inside this process (the loopback
+    transport: every rank gets its own stream and buffers, usually on one
+    device; the ranks' kernels write each other's buffers exactly as they write
+    peer GPUs' memory over NVLink). solve() runs the ranks in one host thread
+    each, like one process per GPU would; every rank returns the same result."""
+
+    def __init__(self, lp: GeneralFormLp, params: SolverParams | None, world: int, devices=None):
+        import dataclasses
+
+        base = params or SolverParams()
+        self.ranks = []
+        for q in range(world):
+            dev = base.device if devices is None else devices[q]
+            p = dataclasses.replace(base, world_size=world, rank=q, device=dev)
+            self.ranks.append(Solver(lp, p))
+        arr = (C.c_void_p * world)(*[r._h for r in self.ranks])
+        _check(self.ranks[0]._lib.pdlp_shard_link_local(arr, world))
+
+    def solve(self) -> list[SolveResult]:
+        import threading
+
+        out: list = [None] * len(self.ranks)
+
+        def run(q):
+            try:
+                out[q] = self.ranks[q].solve()
+            except BaseException as e:  # noqa: BLE001 - re-raised below
+                out[q] = e
+
+        ts = [threading.Thread(target=run, args=(q,)) for q in range(len(self.ranks))]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        for r in out:
+            if isinstance(r, BaseException):
+                raise r
+        return out
+
+    def close(self) -> None:
+        for r in self.ranks:
+            r.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def solve_distributed(lp: GeneralFormLp, params: SolverParams | None = None, group=None) -> SolveResult:
+    """One rank of a row-sharded solve, one process per GPU: rank / world from
+    torch.distributed (any backend; only the CUDA-IPC blobs travel over it),
+    then the ranks exchange data GPU-to-GPU inside the kernels."""
+    import dataclasses
+
+    import torch.distributed as dist
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    base = params or SolverParams()
+    s = Solver(lp, dataclasses.replace(base, world_size=world, rank=rank))
+    try:
+        blobs: list = [None] * world
+        dist.all_gather_object(blobs, s.shard_export(), group=group)
+        s.shard_import(blobs)
+        dist.barrier(group)
+        return s.solve()
+    finally:
+        s.close()
 
 
 MPS_FIXED, MPS_FREE, MPS_AUTO = 0, 1, 2
@@ -266,4 +372,5 @@ def solve(lp: GeneralFormLp, params: SolverParams | None = None) -> SolveResult:
 
 
 __all__ = ["Solver", "solve", "load_library", "default_params", "PdlpError", "library_path", "read_mps",
-           "parse_mps", "write_solution", "MPS_FIXED", "MPS_FREE", "MPS_AUTO"]
+           "parse_mps", "write_solution", "MPS_FIXED", "MPS_FREE", "MPS_AUTO", "ShardGroup", "plan_shards",
+           "solve_distributed"]

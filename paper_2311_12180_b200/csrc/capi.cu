@@ -2,7 +2,9 @@
 // it: std::invalid_argument -> PDLP_EINVAL (the reference's error type for bad
 // input, lp_model.hpp:45-72 / solver.hpp:79-93), CUDA failures -> PDLP_ECUDA,
 // everything else -> PDLP_ERUNTIME; the message is kept per thread.
+#include <algorithm>
 #include <cstring>
+#include <vector>
 #include <limits>
 #include <string>
 
@@ -82,6 +84,9 @@ void pdlp_default_params(pdlp_params* p) {
   p->use_cuda_graph = 1;
   p->l2_persist = 1;
   p->engine = PDLP_ENGINE_AUTO;
+  p->world_size = 1;
+  p->rank = 0;
+  p->plan_world = 0;
 }
 
 int pdlp_create(const pdlp_lp* lp, const pdlp_params* params, pdlp_handle** out) {
@@ -167,5 +172,82 @@ int pdlp_get_sizes(pdlp_handle* h, int64_t* sizes) {
 }
 
 const char* pdlp_last_error(void) { return g_last_error.c_str(); }
+
+// ---- row sharding ------------------------------------------------------
+
+int64_t pdlp_shard_blob_size(void) { return int64_t(sizeof(pdlp::ShardBlob)); }
+
+int pdlp_shard_link_local(pdlp_handle** handles, int32_t world) {
+  if (!handles || world < 1) {
+    g_last_error = "null handles";
+    return PDLP_EINVAL;
+  }
+  return guarded([&] {
+    std::vector<pdlp::Solver*> ranks;
+    for (int q = 0; q < world; ++q) {
+      if (!handles[q]) throw std::invalid_argument("shard link: null handle");
+      ranks.push_back(handles[q]->solver);
+    }
+    pdlp::Solver::link_local(ranks);
+  });
+}
+
+int pdlp_shard_export(pdlp_handle* h, void* blob, int64_t capacity) {
+  if (!h) return null_handle();
+  if (!blob || capacity < int64_t(sizeof(pdlp::ShardBlob))) {
+    g_last_error = "shard export: blob buffer too small";
+    return PDLP_EINVAL;
+  }
+  return guarded([&] { h->solver->export_shard(static_cast<pdlp::ShardBlob*>(blob)); });
+}
+
+int pdlp_shard_import(pdlp_handle* h, const void* blobs, int32_t world) {
+  if (!h) return null_handle();
+  if (!blobs) {
+    g_last_error = "null blobs";
+    return PDLP_EINVAL;
+  }
+  return guarded([&] {
+    std::vector<pdlp::ShardBlob> v(static_cast<size_t>(world));
+    std::memcpy(v.data(), blobs, sizeof(pdlp::ShardBlob) * size_t(world));
+    h->solver->import_shards(v.data(), world);
+  });
+}
+
+int pdlp_shard_info(pdlp_handle* h, int64_t* out) {
+  if (!h) return null_handle();
+  if (!out) {
+    g_last_error = "null output";
+    return PDLP_EINVAL;
+  }
+  return guarded([&] { h->solver->shard_info(out); });
+}
+
+int pdlp_plan_shards(const pdlp_lp* lp, int32_t world, int64_t* k_cuts, int64_t* kt_cuts) {
+  if (!lp || !k_cuts || !kt_cuts) {
+    g_last_error = "null argument";
+    return PDLP_EINVAL;
+  }
+  return guarded([&] {
+    // row offsets of K = vstack(G, A) and of K^T (column counts), on the host
+    const pdlp_csr& G = lp->inequality_matrix;
+    const pdlp_csr& A = lp->equality_matrix;
+    const int64_t m1 = G.num_rows, m2 = A.num_rows, n = lp->num_variables;
+    std::vector<int64_t> rp(size_t(m1 + m2 + 1), 0), rpt(size_t(n + 1), 0);
+    for (int64_t i = 0; i <= m1; ++i) rp[size_t(i)] = G.row_offsets ? G.row_offsets[i] : 0;
+    for (int64_t i = 1; i <= m2; ++i) rp[size_t(m1 + i)] = G.nnz + A.row_offsets[i];
+    for (const pdlp_csr* c : {&G, &A})
+      for (int64_t k = 0; k < c->nnz; ++k) {
+        const int64_t j = c->col_indices ? c->col_indices[k] : c->col_indices32[k];
+        if (j < 0 || j >= n) throw std::invalid_argument("csr: column index out of range");
+        ++rpt[size_t(j) + 1];
+      }
+    for (int64_t j = 0; j < n; ++j) rpt[size_t(j) + 1] += rpt[size_t(j)];
+    const auto kc = pdlp::shard_cuts<int64_t>(m1 + m2, rp.data(), world);
+    const auto ktc = pdlp::shard_cuts<int64_t>(n, rpt.data(), world);
+    std::copy(kc.begin(), kc.end(), k_cuts);
+    std::copy(ktc.begin(), ktc.end(), kt_cuts);
+  });
+}
 
 }  // extern "C"

@@ -56,6 +56,47 @@ struct EvalOut {
   double dx2[2], dy2[2];
 };
 
+// ---------------------------------------------------------------------------
+// Row sharding across ranks (one rank per GPU)
+// ---------------------------------------------------------------------------
+constexpr int kMaxShards = 8;
+
+// Barrier kinds: each participating launch of a producer kernel bumps its
+// local count and publishes it to every peer's flag slot; a consumer waits
+// until every rank's flag reached its own local count (BSP epochs).
+enum SyncKind : int32_t {
+  kSyncDual = 0,    // y', K x' rows, dual partials
+  kSyncPrimal = 1,  // x', primal partials
+  kSyncAvg = 2,     // average slices (once per window, before the evaluation)
+  kSyncEvRows = 3,  // evaluation partials over K
+  kSyncEvCols = 4,  // evaluation partials over K^T (and reduced costs at finish)
+  kSyncKinds = 5
+};
+
+// Per-rank synchronisation block in the rank's own HBM, mapped by the peers.
+struct ShardSync {
+  unsigned long long flag[kSyncKinds][kMaxShards];  // written remotely by rank q
+  unsigned long long count[kSyncKinds];             // local participating launches
+  unsigned ticket[kSyncKinds];                      // local last-CTA tickets
+  int timeout;                                      // a wait gave up (peer lost)
+  int pad;
+};
+
+// Device pointers (valid on this rank: local, or CUDA-IPC-mapped peer memory)
+// of every rank's exchanged buffers. Entry `rank` is the rank's own buffer.
+struct ShardView {
+  double* x_all[kMaxShards];   // the three x buffers, 3 n
+  double* y_all[kMaxShards];   // the three y buffers, 3 m
+  double* d_part[kMaxShards];  // dual partials [K tiles * 3]
+  double* p_part[kMaxShards];  // primal partials [2][K^T tiles * 2]
+  double* avg_x[kMaxShards];
+  double* avg_y[kMaxShards];
+  double* part1[kMaxShards];   // evaluation partials over K
+  double* part2[kMaxShards];   // evaluation partials over K^T
+  double* lam[kMaxShards];     // [4][n] reduced costs
+  ShardSync* sync[kMaxShards];
+};
+
 // Device pointers of one CSR operator with its tile plan.
 struct DevCsr {
   const int* rp;
@@ -65,8 +106,9 @@ struct DevCsr {
   int rows;
   int cols;
   int64_t nnz;
-  const Tile* tiles;
-  int ntiles;
+  const Tile* tiles;       // the GLOBAL tile list of the operator
+  int ntiles;              // tiles this rank runs: tiles[tile0 .. tile0 + ntiles)
+  int tile0;               // global index of the first (partials are indexed globally)
   int chunk_slots;
   double* chunk_part;     // [chunk_slots * 8]
   unsigned* chunk_ctr;    // [split_rows]
@@ -87,14 +129,17 @@ struct DevIter {
   const double* u;
   const double* q;   // scaled rhs (h; b)
   int n, m, m1;
-  int p_grid;        // CTAs of the primal kernel
+  int p_grid;        // CTAs of the primal kernel (own K^T tiles + avg_y blocks)
+  int p_tiles;       // global K^T tiles = primal partials per parity half
   int nonneg;        // every scaled bound is l = +0, u = +inf: clamp is max(v, 0)
   int avg_blocks;    // trailing CTAs of the primal kernel that update avg_y
   double* d_part;    // [K tiles * 3]
   double* p_part;    // [2][p_grid * 2], ping-pong by trial parity
   double* px_total;  // unused (kept for layout stability)
   DevState* snap;    // state the current trial's dual kernel ran on (fast mode)
-  int d_tiles;       // CTAs of the dual kernel (partials the decision sums)
+  int d_tiles;       // global K tiles (dual partials the decision sums)
+  int decide_sep;    // 1: the step decision runs in its own one-CTA kernel (many
+                     //    tiles); 0: every primal CTA recomputes it at its head
   double* seq_dy2;   // parity-mode per-row terms (m)
   double* seq_inter; // (m)
   double* seq_dx2;   // (n)
@@ -102,6 +147,13 @@ struct DevIter {
   const double* gro_tab;  // growth factors 1+(k+1)^-0.6
   void* step_log;         // pdlp_step_log_entry[window capacity]
   DevState* st;
+  // ---- sharding (world == 1: single device, everything below unused) ----
+  int world, rank;
+  int spin;                // 1: consumers wait on peer flags in-kernel (one process per GPU)
+  int row0, row1;          // own rows of K (y, K x, avg_y slices)
+  int col0, col1;          // own rows of K^T = columns (x, K'y, avg_x slices)
+  const ShardView* shv;    // peer table (device memory)
+  ShardSync* sync;         // own sync block
 };
 
 // Vectors of the evaluation block.
@@ -123,6 +175,10 @@ struct DevEval {
   double* seq_r;  // parity: [4][m] row residual terms
   double* seq_d;  // parity: [4][n] column residual terms
   EvalOut* out;
+  int ev1_tiles, ev2_tiles;  // global evaluation tile counts (partials summed)
+  int world, rank;           // sharding (see DevIter)
+  const ShardView* shv;
+  ShardSync* sync;
 };
 
 }  // namespace pdlp

@@ -4,6 +4,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "shard.cuh"
 #include "spmv_engine.cuh"
 
 namespace pdlp {
@@ -46,8 +47,18 @@ __device__ __forceinline__ double2 ldv2(const double* p) {
   return __ldg(reinterpret_cast<const double2*>(p));
 }
 
-template <bool kSeq, bool kCoh = false>
-struct DualEpi : EpiBase<DualEpi<kSeq, kCoh>> {
+// Peer copies of the values an epilogue owns (row sharding, shard.cuh).
+struct PeerPush {
+  double* const* field;  // ShardView pointer array of the exchanged buffer
+  size_t off;            // element offset of the active rotation buffer
+  int world, rank;
+  __device__ __forceinline__ void operator()(int i, double v) const {
+    push_peers(field, world, rank, off + size_t(i), v);
+  }
+};
+
+template <bool kSeq, bool kCoh = false, bool kShard = false>
+struct DualEpi : EpiBase<DualEpi<kSeq, kCoh, kShard>> {
   static constexpr int NP = 1, NA = 1, NR = 3;
   static constexpr TileGeom kGeom = kIterGeom;
   static constexpr bool kNeedCol = false;
@@ -61,6 +72,7 @@ struct DualEpi : EpiBase<DualEpi<kSeq, kCoh>> {
   double* __restrict__ seq_inter;
   double sigma;
   int m1;
+  PeerPush push;  // y' to every peer (kShard)
   __device__ __forceinline__ void gather(int c, double (&g)[1]) const { g[0] = ldv<kCoh>(xg + c); }
   __device__ __forceinline__ void add(double (&a)[1], const double (&p)[1], int) const { a[0] += p[0]; }
   __device__ __forceinline__ void row_done(int r, const double (&a)[1], double (&red)[3]) const {
@@ -69,6 +81,7 @@ struct DualEpi : EpiBase<DualEpi<kSeq, kCoh>> {
     double yn = yo + sigma * (q[r] - 2.0 * kxn + kxo);  // solver.hpp:412-413
     if (r < m1 && yn < 0.0) yn = 0.0;                    // project_dual_in_place
     yt[r] = yn;
+    if (kShard) push(r, yn);
     kxt[r] = kxn;
     const double d = yn - yo;
     const double dd = d * d, di = d * (kxn - kxo);
@@ -102,6 +115,7 @@ struct DualEpi : EpiBase<DualEpi<kSeq, kCoh>> {
         double yn = yo[i] + sigma * (qq[i] - 2.0 * kxn + kxo[i]);  // solver.hpp:412-413
         if (r < m1 && yn < 0.0) yn = 0.0;
         yt[r] = yn;
+        if (kShard) push(r, yn);
         kxt[r] = kxn;
         const double d = yn - yo[i];
         const double dd = d * d, di = d * (kxn - kxo[i]);
@@ -116,8 +130,8 @@ struct DualEpi : EpiBase<DualEpi<kSeq, kCoh>> {
   }
 };
 
-template <bool kSeq, bool kNonneg, bool kCoh = false>
-struct PrimalEpi : EpiBase<PrimalEpi<kSeq, kNonneg, kCoh>> {
+template <bool kSeq, bool kNonneg, bool kCoh = false, bool kShard = false>
+struct PrimalEpi : EpiBase<PrimalEpi<kSeq, kNonneg, kCoh, kShard>> {
   static constexpr int NP = 1, NA = 1, NR = 2;
   static constexpr TileGeom kGeom = kIterGeom;
   static constexpr bool kNeedCol = false;
@@ -134,6 +148,7 @@ struct PrimalEpi : EpiBase<PrimalEpi<kSeq, kNonneg, kCoh>> {
   double ratio;
   int do_avg;
   int avg_first;
+  PeerPush push;  // x' to every peer (kShard)
   __device__ __forceinline__ void gather(int r, double (&g)[1]) const { g[0] = ldv<kCoh>(yg + r); }
   __device__ __forceinline__ void add(double (&a)[1], const double (&p)[1], int) const { a[0] += p[0]; }
   __device__ __forceinline__ void row_done(int j, const double (&a)[1], double (&red)[2]) const {
@@ -144,6 +159,7 @@ struct PrimalEpi : EpiBase<PrimalEpi<kSeq, kNonneg, kCoh>> {
     const double v = xa - tau * (c[j] - s);  // solver.hpp:404-408
     const double xn = kNonneg ? smax(v, 0.0) : clamp_box(v, l[j], u[j]);
     xt[j] = xn;
+    if (kShard) push(j, xn);
     const double d = xn - xa;
     const double dd = d * d;
     if (kSeq) seq_dx2[j] = dd;
@@ -189,6 +205,8 @@ struct PrimalEpi : EpiBase<PrimalEpi<kSeq, kNonneg, kCoh>> {
     }
     st2(kty_out + j0, s4);
     st2(xt + j0, xn4);
+    if (kShard)
+      for (int i = 0; i < 4; ++i) push(j0 + i, xn4[i]);
     if (do_avg) st2(avg_x + j0, av);
   }
   // all operand loads of the thread's columns first, then the updates (ILP)
@@ -219,6 +237,7 @@ struct PrimalEpi : EpiBase<PrimalEpi<kSeq, kNonneg, kCoh>> {
         const double v = xa[i] - tau * (cc[i] - s);  // solver.hpp:404-408
         const double xn = kNonneg ? smax(v, 0.0) : clamp_box(v, ll[i], uu[i]);
         xt[j] = xn;
+        if (kShard) push(j, xn);
         const double d = xn - xa[i];
         const double dd = d * d;
         if (kSeq) seq_dx2[j] = dd;

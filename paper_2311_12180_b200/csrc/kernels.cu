@@ -18,6 +18,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
 #include <utility>
 
 #include "../../include/pdlp_b200.h"
@@ -164,32 +165,40 @@ __device__ Decision step_decision(const DevState& s, const DevIter& it, double d
 // the same order), so this kernel has no serial tail; CTA 0 snapshots the state
 // the decision will start from. Parity mode keeps the decision here (last CTA),
 // where the reference-order sequential sums run.
-template <bool kSeq>
+template <bool kSeq, bool kShard>
 __global__ void __launch_bounds__(kThreads, 4) dual_kernel(DevCsr K, DevIter it,
                                                            cudaGraphConditionalHandle cond,
                                                            int use_cond) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const Tile t = K.tiles[blockIdx.x];
+  const int tile = K.tile0 + int(blockIdx.x);  // global tile index (partials, sharding)
+  const Tile t = K.tiles[tile];
   prefetch_tile(t, K.rp, K.col, K.val);
   griddep_wait();  // x' and the state come from the previous primal kernel
   DevState* st = it.st;
+  // A failed or completed window parks the remaining (stream-engine) launches;
+  // parking is decided from state that is identical on every rank.
+  bool parked = st->failure || st->window_accepts >= st->window_target;
+  if (kShard && !parked && !shard_wait(it.sync, it.world, kSyncPrimal)) {
+    // a peer never published its x' slice: end the solve with a numerical error
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->failure = 1;
+    parked = true;
+  }
   if (!kSeq && blockIdx.x == 0) {
     if (threadIdx.x == 0) *it.snap = *st;
     // the primal partials of x' (the decision's dx^2) are reduced here, off the
     // critical path, so the decision at the primal head has one round trip
     double pp[2];
-    sum_partials<2, 0>(it.p_part + size_t(st->trials_total & 1) * it.p_grid * 2, it.p_grid, pp);
+    sum_partials<2, 0>(it.p_part + size_t(st->trials_total & 1) * it.p_tiles * 2, it.p_tiles, pp);
     if (threadIdx.x == 0) {
       it.px_total[0] = pp[0];
       it.px_total[1] = pp[1];
     }
   }
-  // A failed or completed window parks the remaining (stream-engine) launches.
-  if (st->failure || st->window_accepts >= st->window_target) {
+  if (parked) {
     if (kSeq && blockIdx.x == 0 && threadIdx.x == 0) st->p_mode = kPNone;
     return;
   }
-  DualEpi<kSeq> epi;
+  DualEpi<kSeq, false, kShard> epi;
   epi.xg = it.x[st->ix_trial];
   epi.y = it.y[st->iy_cur];
   epi.kx = it.kx[st->ikx_cur];
@@ -200,19 +209,26 @@ __global__ void __launch_bounds__(kThreads, 4) dual_kernel(DevCsr K, DevIter it,
   epi.seq_inter = it.seq_inter;
   epi.sigma = st->eta * st->omega;  // sigma = eta * omega, solver.hpp:402
   epi.m1 = it.m1;
+  if (kShard) epi.push = PeerPush{it.shv->y_all, size_t(st->iy_trial) * it.m, it.world, it.rank};
   double red[3] = {0.0, 0.0, 0.0};
-  run_tile<DualEpi<kSeq>, kSeq>(t, K.rp, K.col, K.val, epi, red, K.chunk_part, K.chunk_ctr, smem);
+  run_tile<DualEpi<kSeq, false, kShard>, kSeq>(t, K.rp, K.col, K.val, epi, red, K.chunk_part,
+                                               K.chunk_ctr, smem);
   // the primal kernel's CTAs may start their prologue once every dual CTA is
   // past its tile (triggering earlier would let them take slots from our waves)
   griddep_launch_dependents();
-  store_partial<3, 0>(red, it.d_part, blockIdx.x);
+  store_partial<3, 0>(red, it.d_part, tile);
+  if (kShard) {
+    push_partial<3>(it.shv->d_part, it.world, it.rank, 0, size_t(tile), red);
+    shard_signal(it.shv, it.sync, it.world, it.rank, kSyncDual);
+    return;
+  }
   if (!kSeq) return;
 
   // ---- parity mode: the decision in the last CTA, sums in reference order ----
   if (!grid_last_block(&st->ctr_dual, gridDim.x)) return;
   double dpart[3], ppart[2];
-  sum_partials<3, 0>(it.d_part, gridDim.x, dpart);
-  sum_partials<2, 0>(it.p_part + size_t(st->trials_total & 1) * it.p_grid * 2, it.p_grid, ppart);
+  sum_partials<3, 0>(it.d_part, it.d_tiles, dpart);
+  sum_partials<2, 0>(it.p_part + size_t(st->trials_total & 1) * it.p_tiles * 2, it.p_tiles, ppart);
   if (threadIdx.x != 0) return;
   const double dx2 = seq_sum(it.seq_dx2, it.n);  // solver.hpp:422-435
   double dy2 = 0.0, inter = 0.0;
@@ -235,21 +251,24 @@ __global__ void __launch_bounds__(kThreads, 4) dual_kernel(DevCsr K, DevIter it,
 // Primal side of a trial. mode_override >= 0 forces a branch (first trial of a
 // solve: retry; after a restart: restart). Otherwise the fast mode takes the
 // step decision first (all CTAs, CTA 0 commits it), parity mode reads it.
-template <bool kSeq, bool kNonneg>
+template <bool kSeq, bool kNonneg, bool kShard>
 __global__ void __launch_bounds__(kThreads, 4) primal_kernel(DevCsr KT, DevIter it, int mode_override,
                                                              cudaGraphConditionalHandle cond,
                                                              int use_cond) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Decision sd;
-  if (int(blockIdx.x) < KT.ntiles) {
-    const Tile tp = KT.tiles[blockIdx.x];
+  const int bid = blockIdx.x;
+  const int tile = KT.tile0 + bid;  // global tile index (CTAs >= ntiles: avg_y slices)
+  if (bid < KT.ntiles) {
+    const Tile tp = KT.tiles[tile];
     prefetch_tile(tp, KT.rp, KT.col, KT.val);
   }
   griddep_wait();  // y' and the dual partials come from the dual kernel
   DevState* st = it.st;
-  const int bid = blockIdx.x;
   Decision d;
-  if (mode_override >= 0 || kSeq) {
+  if (mode_override >= 0 || kSeq || it.decide_sep) {
+    // forced branch, or the decision was committed to the state already
+    // (parity mode: the dual's last CTA; many tiles: decide_kernel)
     const DevState& s = *st;
     d.mode = mode_override >= 0 ? mode_override : s.p_mode;
     d.eta = s.eta;
@@ -261,10 +280,12 @@ __global__ void __launch_bounds__(kThreads, 4) primal_kernel(DevCsr KT, DevIter 
   } else {
     // decision inputs, all issued as independent loads (one round trip): the
     // state snapshot the dual kernel ran on, the window's step-factor table,
-    // the pre-reduced dx^2, and the dual partials
+    // the pre-reduced dx^2, and the dual partials (sharded: after every rank
+    // published its partials)
     __shared__ DevState s_snap;
     __shared__ double s_tab[2][kHeadTab];
     __shared__ double s_px[2];
+    __shared__ double s_dp[3];
     constexpr int kWords = int(sizeof(DevState) / sizeof(unsigned long long));
     const int tid = threadIdx.x;
     unsigned long long w = 0;
@@ -276,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, 4) primal_kernel(DevCsr KT, DevIter 
     }
     if (tid < 2) px = __ldcg(it.px_total + tid);
     double dp[3];
-    sum_partials<3, 0>(it.d_part, it.d_tiles, dp);
+    if (!kShard) sum_partials<3, 0>(it.d_part, it.d_tiles, dp);
     if (tid < kWords) reinterpret_cast<unsigned long long*>(&s_snap)[tid] = w;
     if (tid < kHeadTab) {
       s_tab[0][tid] = tr;
@@ -284,9 +305,21 @@ __global__ void __launch_bounds__(kThreads, 4) primal_kernel(DevCsr KT, DevIter 
     }
     if (tid < 2) s_px[tid] = px;
     __syncthreads();
+    bool parked = s_snap.failure || s_snap.window_accepts >= s_snap.window_target;
+    if (kShard && !parked) {
+      if (!shard_wait(it.sync, it.world, kSyncDual)) {
+        if (bid == 0 && tid == 0) st->failure = 1;
+        parked = true;
+      } else {
+        sum_partials<3, 0>(it.d_part, it.d_tiles, dp);
+        if (tid == 0) s_dp[0] = dp[0], s_dp[1] = dp[1], s_dp[2] = dp[2];
+        __syncthreads();
+        dp[0] = s_dp[0], dp[1] = s_dp[1], dp[2] = s_dp[2];
+      }
+    }
     if (tid == 0) {
       const DevState& s = s_snap;
-      if (s.failure || s.window_accepts >= s.window_target) {
+      if (parked) {
         sd.mode = kPNone;  // parked launch of a completed window (stream engine)
       } else {
         const bool commit = bid == 0;
@@ -308,54 +341,61 @@ __global__ void __launch_bounds__(kThreads, 4) primal_kernel(DevCsr KT, DevIter 
   if (d.mode == kPNone) return;  // keep the partials of the last real trial
   double red[2] = {0.0, 0.0};
   const double tau = d.eta / d.omega;  // tau = eta / omega, solver.hpp:401
-  if (d.mode == kPAccept || d.mode == kPRestart) {
-    const bool acc = d.mode == kPAccept;
-    if (bid < KT.ntiles) {
-      {
-        // the epilogue's contiguous operands of this tile's columns -> L2 while
-        // the matrix and the gathers are in flight
-        const Tile tt = KT.tiles[bid];
-        const int j0 = tt.kind == kTileChunk ? tt.row0 : tt.row0;
-        const int j1 = tt.kind == kTileChunk ? tt.row0 + 1 : tt.row1;
-        for (int j = (j0 & ~15) + 16 * int(threadIdx.x); j < j1; j += 16 * kThreads) {
-          prefetch_l2(it.x[d.ix_cur] + j);
-          prefetch_l2(it.c + j);
-          if (acc) prefetch_l2(it.avg_x + j);
-          if (!kNonneg) {
-            prefetch_l2(it.l + j);
-            prefetch_l2(it.u + j);
-          }
-        }
-      }
-      PrimalEpi<kSeq, kNonneg> epi;
-      epi.yg = it.y[d.iy_cur];
-      epi.xc = it.x[d.ix_cur];
-      epi.c = it.c;
-      epi.l = it.l;
-      epi.u = it.u;
-      epi.kty_out = it.kty[d.ikty_cur];
-      epi.xt = it.x[d.ix_trial];
-      epi.avg_x = it.avg_x;
-      epi.seq_dx2 = it.seq_dx2;
-      epi.tau = tau;
-      epi.ratio = d.ratio;
-      epi.do_avg = acc;
-      epi.avg_first = d.first;
-      const Tile t = KT.tiles[bid];
-      run_tile<PrimalEpi<kSeq, kNonneg>, kSeq>(t, KT.rp, KT.col, KT.val, epi, red, KT.chunk_part,
-                                               KT.chunk_ctr, smem);
-    } else if (acc) {
-      // avg_y .add (solver.hpp:839) on this CTA's slice of the dual vector
+  const PeerPush push{kShard ? it.shv->x_all : nullptr, size_t(d.ix_trial) * it.n, it.world, it.rank};
+  if (bid >= KT.ntiles) {
+    // avg_y .add (solver.hpp:839) on this CTA's slice of the own dual rows; no partial
+    if (d.mode == kPAccept) {
       const int nb = it.avg_blocks, b = bid - KT.ntiles;
-      const int per = (it.m + nb - 1) / nb;
-      const int i0 = b * per, i1 = min(it.m, i0 + per);
+      const int rows = it.row1 - it.row0;
+      const int per = (rows + nb - 1) / nb;
+      const int i0 = it.row0 + b * per, i1 = min(it.row1, i0 + per);
       const double* yc = it.y[d.iy_cur];
       for (int i = i0 + threadIdx.x; i < i1; i += kThreads)
         it.avg_y[i] = d.first ? yc[i] : it.avg_y[i] + d.ratio * (yc[i] - it.avg_y[i]);
     }
+    if (kShard) shard_signal(it.shv, it.sync, it.world, it.rank, kSyncPrimal);
+    return;
+  }
+  const Tile t = KT.tiles[tile];
+  if (d.mode == kPAccept || d.mode == kPRestart) {
+    const bool acc = d.mode == kPAccept;
+    {
+      // the epilogue's contiguous operands of this tile's columns -> L2 while
+      // the matrix and the gathers are in flight
+      const int j0 = t.row0;
+      const int j1 = t.kind == kTileChunk ? t.row0 + 1 : t.row1;
+      for (int j = (j0 & ~15) + 16 * int(threadIdx.x); j < j1; j += 16 * kThreads) {
+        prefetch_l2(it.x[d.ix_cur] + j);
+        prefetch_l2(it.c + j);
+        if (acc) prefetch_l2(it.avg_x + j);
+        if (!kNonneg) {
+          prefetch_l2(it.l + j);
+          prefetch_l2(it.u + j);
+        }
+      }
+    }
+    PrimalEpi<kSeq, kNonneg, false, kShard> epi;
+    epi.yg = it.y[d.iy_cur];
+    epi.xc = it.x[d.ix_cur];
+    epi.c = it.c;
+    epi.l = it.l;
+    epi.u = it.u;
+    epi.kty_out = it.kty[d.ikty_cur];
+    epi.xt = it.x[d.ix_trial];
+    epi.avg_x = it.avg_x;
+    epi.seq_dx2 = it.seq_dx2;
+    epi.tau = tau;
+    epi.ratio = d.ratio;
+    epi.do_avg = acc;
+    epi.avg_first = d.first;
+    epi.push = push;
+    run_tile<PrimalEpi<kSeq, kNonneg, false, kShard>, kSeq>(t, KT.rp, KT.col, KT.val, epi, red,
+                                                            KT.chunk_part, KT.chunk_ctr, smem);
   } else if (d.mode == kPRetry) {
-    const int per = (it.n + gridDim.x - 1) / gridDim.x;
-    const int j0 = bid * per, j1 = min(it.n, j0 + per);
+    // x' for the shrunk step over this tile's columns (a split column is
+    // handled by its first slice), so the partials keep the tile layout
+    const int j0 = t.row0;
+    const int j1 = t.kind == kTileChunk ? (t.part == 0 ? t.row0 + 1 : t.row0) : t.row1;
     const double* xc = it.x[d.ix_cur];
     const double* kty = it.kty[d.ikty_cur];
     double* xt = it.x[d.ix_trial];
@@ -364,6 +404,7 @@ __global__ void __launch_bounds__(kThreads, 4) primal_kernel(DevCsr KT, DevIter 
       const double v = xa - tau * (it.c[j] - kty[j]);
       const double xn = kNonneg ? smax(v, 0.0) : clamp_box(v, it.l[j], it.u[j]);
       xt[j] = xn;
+      if (kShard) push(j, xn);
       const double dd = (xn - xa) * (xn - xa);
       if (kSeq) it.seq_dx2[j] = dd;
       red[0] += dd;
@@ -373,7 +414,47 @@ __global__ void __launch_bounds__(kThreads, 4) primal_kernel(DevCsr KT, DevIter 
   griddep_launch_dependents();
   // ping-pong by trial parity: the next decision reads these while this launch's
   // late CTAs may still be reading the previous ones
-  store_partial<2, 0>(red, it.p_part + size_t(d.trials & 1) * it.p_grid * 2, bid);
+  const size_t half = size_t(d.trials & 1) * it.p_tiles * 2;
+  store_partial<2, 0>(red, it.p_part + half, tile);
+  if (kShard) {
+    push_partial<2>(it.shv->p_part, it.world, it.rank, half, size_t(tile), red);
+    shard_signal(it.shv, it.sync, it.world, it.rank, kSyncPrimal);
+  }
+}
+
+// Step decision as its own one-CTA kernel between the dual and the primal
+// kernel, used when the operator has so many tiles that recomputing it in every
+// primal CTA would cost more than a launch (sum_partials over all dual
+// partials per CTA). Same sums in the same order as the primal-head variant,
+// so both give bitwise identical decisions.
+template <bool kShard>
+__global__ void __launch_bounds__(kThreads) decide_kernel(DevIter it, cudaGraphConditionalHandle cond,
+                                                          int use_cond) {
+  griddep_wait();
+  DevState* st = it.st;
+  if (st->failure || st->window_accepts >= st->window_target) {
+    if (threadIdx.x == 0) st->p_mode = kPNone;
+    return;
+  }
+  if (kShard && !shard_wait(it.sync, it.world, kSyncDual)) {
+    if (threadIdx.x == 0) {
+      st->failure = 1;
+      st->p_mode = kPNone;
+      if (use_cond) cudaGraphSetConditional(cond, 0u);
+    }
+    return;
+  }
+  double dp[3];
+  sum_partials<3, 0>(it.d_part, it.d_tiles, dp);
+  griddep_launch_dependents();
+  if (threadIdx.x != 0) return;
+  const DevState pre = *st;
+  const int64_t ti = pre.total - pre.table_base;
+  const double px0 = __ldcg(it.px_total), px1 = __ldcg(it.px_total + 1);
+  const Decision d = step_decision(pre, it, dp[0], dp[1], px0, dp[2] == 0.0 && px1 == 0.0,
+                                   it.red_tab[ti], it.gro_tab[ti], st);
+  __threadfence();
+  if (use_cond) cudaGraphSetConditional(cond, d.cont ? 1u : 0u);
 }
 
 // ===========================================================================
@@ -401,7 +482,7 @@ __global__ void __launch_bounds__(kThreads) spmv_kernel(DevCsr A, const double* 
   epi.x = x;
   epi.out = out;
   double red[1] = {0.0};
-  const Tile t = A.tiles[blockIdx.x];
+  const Tile t = A.tiles[A.tile0 + blockIdx.x];
   run_tile<MatvecEpi, kSeq>(t, A.rp, A.col, val, epi, red, A.chunk_part, A.chunk_ctr, smem);
 }
 
@@ -455,6 +536,9 @@ __global__ void restart_copy_kernel(DevIter it, int from_avg) {
 constexpr int kEv0Items = 4;  // elements per thread per block pass
 
 __global__ void __launch_bounds__(kThreads) eval_prep_kernel(DevIter it, DevEval ev, int xblocks) {
+  // sharded: every rank evaluates the four points redundantly on full vectors,
+  // once the peers' average slices arrived (push_avg_kernel)
+  if (it.world > 1) shard_wait(it.sync, it.world, kSyncAvg);
   const DevState* st = it.st;
   const bool empty = st->wsum == 0.0;
   const double inv_t = st->inner > 0 ? 1.0 / double(st->inner) : 0.0;
@@ -497,6 +581,23 @@ __global__ void __launch_bounds__(kThreads) eval_prep_kernel(DevIter it, DevEval
     }
   }
   store_partial<4, 0>(red, ev.part0, blockIdx.x);
+}
+
+// Sharded evaluation: this rank's slices of the averages to every peer (the
+// iteration keeps averages rank-local; they are gathered once per window).
+__global__ void push_avg_kernel(DevIter it) {
+  const ShardView* v = it.shv;
+  const int stride = gridDim.x * blockDim.x;
+  for (int j = it.col0 + blockIdx.x * blockDim.x + threadIdx.x; j < it.col1; j += stride)
+    push_peers(v->avg_x, it.world, it.rank, size_t(j), it.avg_x[j]);
+  for (int i = it.row0 + blockIdx.x * blockDim.x + threadIdx.x; i < it.row1; i += stride)
+    push_peers(v->avg_y, it.world, it.rank, size_t(i), it.avg_y[i]);
+  shard_signal(v, it.sync, it.world, it.rank, kSyncAvg);
+}
+
+// Waits (on the device) until every rank published `kind`.
+__global__ void shard_barrier_kernel(ShardSync* sync, int world, int kind) {
+  shard_wait(sync, world, kind);
 }
 
 int eval_grid0(int n, int m) {
@@ -589,6 +690,7 @@ struct Ev2Epi : EpiBase<Ev2Epi<kSeq>> {
   double* __restrict__ seq_d;
   int n, m1;
   int lam_slot;  // slot whose reduced costs are stored (-1: none; parity mode: all)
+  PeerPush lam_push;  // sharded finish: the stored slot's reduced costs to every peer
   __device__ __forceinline__ void gather(int r, double (&g)[4]) const { load4(Y4 + size_t(r) * 4, g); }
   __device__ __forceinline__ void add(double (&a)[8], const double (&p)[4], int col) const {
     if (col < m1) {
@@ -607,7 +709,10 @@ struct Ev2Epi : EpiBase<Ev2Epi<kSeq>> {
     for (int s = 0; s < 2; ++s) {
       const double slack = (cj + -1.0 * a[s]) + -1.0 * a[4 + s];
       const double lm = reduced_cost(slack, lj, uj);
-      if (kSeq || s == lam_slot) lam[size_t(s) * n + j] = lm;
+      if (kSeq || s == lam_slot) {
+        lam[size_t(s) * n + j] = lm;
+        if (s == lam_slot && lam_push.world > 1) lam_push(s * n + j, lm);
+      }
       const double dres = slack + -1.0 * lm;
       if (kSeq) seq_d[size_t(s) * n + j] = dres;
       red[s * 3 + 0] += dres * dres;
@@ -618,7 +723,10 @@ struct Ev2Epi : EpiBase<Ev2Epi<kSeq>> {
     for (int s = 2; s < 4; ++s) {
       const double kty = a[s] + 1.0 * a[4 + s];
       const double lm = reduced_cost(-kty, lj, uj);
-      if (kSeq || s == lam_slot) lam[size_t(s) * n + j] = lm;
+      if (kSeq || s == lam_slot) {
+        lam[size_t(s) * n + j] = lm;
+        if (s == lam_slot && lam_push.world > 1) lam_push(s * n + j, lm);
+      }
       const double viol = kty + 1.0 * lm;
       if (kSeq) seq_d[size_t(s) * n + j] = viol;
       const int o = 6 + (s - 2) * 4;
@@ -641,11 +749,15 @@ __global__ void __launch_bounds__(kThreads) eval_rows_kernel(DevCsr K, DevEval e
   double red[14];
 #pragma unroll
   for (int i = 0; i < 14; ++i) red[i] = i < 12 ? 0.0 : -INFINITY;
-  // each CTA walks several tiles, so the final reduction sums one partial per CTA
-  for (int ti = blockIdx.x; ti < K.ntiles; ti += gridDim.x)
-    run_tile<Ev1Epi<kSeq>, kSeq>(K.tiles[ti], K.rp, K.col, K.val_orig, epi, red, K.chunk_part,
-                                 K.chunk_ctr, smem);
-  store_partial<12, 2>(red, ev.part1, blockIdx.x);
+  // one tile per CTA, one partial per (global) tile
+  const int ti = K.tile0 + int(blockIdx.x);
+  run_tile<Ev1Epi<kSeq>, kSeq>(K.tiles[ti], K.rp, K.col, K.val_orig, epi, red, K.chunk_part,
+                               K.chunk_ctr, smem);
+  store_partial<12, 2>(red, ev.part1, ti);
+  if (ev.world > 1) {
+    push_partial<14>(ev.shv->part1, ev.world, ev.rank, 0, size_t(ti), red);
+    shard_signal(ev.shv, ev.sync, ev.world, ev.rank, kSyncEvRows);
+  }
 }
 
 template <bool kSeq>
@@ -658,10 +770,15 @@ __global__ void __launch_bounds__(kThreads) eval_cols_kernel(DevCsr KT, DevEval 
   double red[18];
 #pragma unroll
   for (int i = 0; i < 18; ++i) red[i] = i < 14 ? 0.0 : -INFINITY;
-  for (int ti = blockIdx.x; ti < KT.ntiles; ti += gridDim.x)
-    run_tile<Ev2Epi<kSeq>, kSeq>(KT.tiles[ti], KT.rp, KT.col, KT.val_orig, epi, red, KT.chunk_part,
-                                 KT.chunk_ctr, smem);
-  store_partial<14, 4>(red, ev.part2, blockIdx.x);
+  epi.lam_push = PeerPush{ev.shv ? ev.shv->lam : nullptr, 0, ev.world, ev.rank};
+  const int ti = KT.tile0 + int(blockIdx.x);
+  run_tile<Ev2Epi<kSeq>, kSeq>(KT.tiles[ti], KT.rp, KT.col, KT.val_orig, epi, red, KT.chunk_part,
+                               KT.chunk_ctr, smem);
+  store_partial<14, 4>(red, ev.part2, ti);
+  if (ev.world > 1) {
+    push_partial<18>(ev.shv->part2, ev.world, ev.rank, 0, size_t(ti), red);
+    shard_signal(ev.shv, ev.sync, ev.world, ev.rank, kSyncEvCols);
+  }
 }
 
 // Parity-mode dual objective: the single sequential accumulator of
@@ -682,6 +799,10 @@ template <bool kSeq>
 __global__ void __launch_bounds__(kThreads) eval_final_kernel(DevEval ev, int grid1, int grid2,
                                                               int n, int m, int m1) {
   double p0[4], p1[14], p2[18];
+  if (ev.world > 1) {
+    shard_wait(ev.sync, ev.world, kSyncEvRows);
+    shard_wait(ev.sync, ev.world, kSyncEvCols);
+  }
   sum_partials<4, 0>(ev.part0, ev.grid0, p0);
   sum_partials<12, 2>(ev.part1, grid1, p1);
   sum_partials<14, 4>(ev.part2, grid2, p2);
@@ -1114,9 +1235,19 @@ void launch_dual(const DevCsr& k, const DevIter& it, bool seq, unsigned long lon
   const size_t sm = stream_smem_bytes<DualEpi<false>>();
   cudaGraphConditionalHandle h = static_cast<cudaGraphConditionalHandle>(cond);
   if (seq)
-    launch_pdl(dual_kernel<true>, k.ntiles, sm, s, k, it, h, use_cond);
+    launch_pdl(dual_kernel<true, false>, k.ntiles, sm, s, k, it, h, use_cond);
+  else if (it.world > 1)
+    launch_pdl(dual_kernel<false, true>, k.ntiles, sm, s, k, it, h, use_cond);
   else
-    launch_pdl(dual_kernel<false>, k.ntiles, sm, s, k, it, h, use_cond);
+    launch_pdl(dual_kernel<false, false>, k.ntiles, sm, s, k, it, h, use_cond);
+}
+
+void launch_decide(const DevIter& it, cudaStream_t s, unsigned long long cond, int use_cond) {
+  cudaGraphConditionalHandle h = static_cast<cudaGraphConditionalHandle>(cond);
+  if (it.world > 1)
+    launch_pdl(decide_kernel<true>, 1, 0, s, it, h, use_cond);
+  else
+    launch_pdl(decide_kernel<false>, 1, 0, s, it, h, use_cond);
 }
 
 void launch_primal(const DevCsr& kt, const DevIter& it, bool seq, int mode_override,
@@ -1125,14 +1256,19 @@ void launch_primal(const DevCsr& kt, const DevIter& it, bool seq, int mode_overr
   const size_t sm = stream_smem_bytes<PrimalEpi<false, false>>();
   if (seq) {
     if (it.nonneg)
-      launch_pdl(primal_kernel<true, true>, it.p_grid, sm, s, kt, it, mode_override, h, use_cond);
+      launch_pdl(primal_kernel<true, true, false>, it.p_grid, sm, s, kt, it, mode_override, h, use_cond);
     else
-      launch_pdl(primal_kernel<true, false>, it.p_grid, sm, s, kt, it, mode_override, h, use_cond);
+      launch_pdl(primal_kernel<true, false, false>, it.p_grid, sm, s, kt, it, mode_override, h, use_cond);
+  } else if (it.world > 1) {
+    if (it.nonneg)
+      launch_pdl(primal_kernel<false, true, true>, it.p_grid, sm, s, kt, it, mode_override, h, use_cond);
+    else
+      launch_pdl(primal_kernel<false, false, true>, it.p_grid, sm, s, kt, it, mode_override, h, use_cond);
   } else {
     if (it.nonneg)
-      launch_pdl(primal_kernel<false, true>, it.p_grid, sm, s, kt, it, mode_override, h, use_cond);
+      launch_pdl(primal_kernel<false, true, false>, it.p_grid, sm, s, kt, it, mode_override, h, use_cond);
     else
-      launch_pdl(primal_kernel<false, false>, it.p_grid, sm, s, kt, it, mode_override, h, use_cond);
+      launch_pdl(primal_kernel<false, false, false>, it.p_grid, sm, s, kt, it, mode_override, h, use_cond);
   }
 }
 
@@ -1149,9 +1285,14 @@ void launch_restart_copy(const DevIter& it, int from_avg, cudaStream_t s) {
 int eval_grid(int ntiles) { return ntiles; }  // one tile per CTA: short latency chains
 
 void launch_eval(const DevCsr& k, const DevCsr& kt, const DevIter& it, const DevEval& ev, bool seq,
-                 cudaStream_t s) {
+                 cudaStream_t s, const PhaseFn& phase) {
   const int span = kThreads * kEv0Items;
   const int xblocks = ceil_div(it.n, span);
+  if (it.world > 1) {  // the average slices to every rank, then the redundant EV0
+    push_avg_kernel<<<grid_for(std::max(it.col1 - it.col0, it.row1 - it.row0)), kThreads, 0, s>>>(it);
+    PDLP_CUDA(cudaGetLastError());
+    if (phase) phase();
+  }
   eval_prep_kernel<<<ev.grid0, kThreads, 0, s>>>(it, ev, xblocks);
   PDLP_CUDA(cudaGetLastError());
   const size_t sm1 = stream_smem_bytes<Ev1Epi<false>>();
@@ -1160,22 +1301,29 @@ void launch_eval(const DevCsr& k, const DevCsr& kt, const DevIter& it, const Dev
   if (seq) {
     eval_rows_kernel<true><<<g1, kThreads, sm1, s>>>(k, ev, it.m, it.m1);
     eval_cols_kernel<true><<<g2, kThreads, sm2, s>>>(kt, ev, it.n, it.m1, -1);
-    eval_final_kernel<true><<<1, kThreads, 0, s>>>(ev, g1, g2, it.n, it.m, it.m1);
+    eval_final_kernel<true><<<1, kThreads, 0, s>>>(ev, ev.ev1_tiles, ev.ev2_tiles, it.n, it.m, it.m1);
     eval_seq_displacement_kernel<<<1, 32, 0, s>>>(it, ev.out);
   } else {
     eval_rows_kernel<false><<<g1, kThreads, sm1, s>>>(k, ev, it.m, it.m1);
     eval_cols_kernel<false><<<g2, kThreads, sm2, s>>>(kt, ev, it.n, it.m1, -1);
-    eval_final_kernel<false><<<1, kThreads, 0, s>>>(ev, g1, g2, it.n, it.m, it.m1);
+    PDLP_CUDA(cudaGetLastError());
+    if (it.world > 1 && phase) phase();
+    eval_final_kernel<false><<<1, kThreads, 0, s>>>(ev, ev.ev1_tiles, ev.ev2_tiles, it.n, it.m, it.m1);
   }
   PDLP_CUDA(cudaGetLastError());
 }
 
 void launch_eval_lambda(const DevCsr& kt, const DevIter& it, const DevEval& ev, bool seq, int slot,
-                        cudaStream_t s) {
+                        cudaStream_t s, const PhaseFn& phase) {
   if (seq) return;  // parity mode stores every slot's reduced costs on each evaluation
   const size_t sm2 = stream_smem_bytes<Ev2Epi<false>>();
   eval_cols_kernel<false><<<eval_grid(kt.ntiles), kThreads, sm2, s>>>(kt, ev, it.n, it.m1, slot);
   PDLP_CUDA(cudaGetLastError());
+  if (it.world > 1) {  // wait for every rank's slice of the reduced costs
+    if (phase) phase();
+    shard_barrier_kernel<<<1, 32, 0, s>>>(ev.sync, ev.world, int(kSyncEvCols));
+    PDLP_CUDA(cudaGetLastError());
+  }
 }
 
 void launch_reduced_of_objective(const double* c, const double* l, const double* u, int n,

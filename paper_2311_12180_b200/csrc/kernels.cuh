@@ -3,9 +3,15 @@
 
 #include <cuda_runtime.h>
 
+#include <functional>
+
 #include "device_state.h"
 
 namespace pdlp {
+
+// Host hook run after each launch whose outputs peers consume (sharded runs in
+// one process order their ranks' streams through it; empty otherwise).
+using PhaseFn = std::function<void()>;
 
 // ---- setup -----------------------------------------------------------------
 void launch_build_rowptr(const int64_t* g_off, const int64_t* a_off, int64_t m1, int64_t m2,
@@ -48,6 +54,8 @@ void launch_spmv(const DevCsr& a, bool orig_vals, const double* x, double* out, 
 // step decision; sets the WHILE condition when `cond` != 0.
 void launch_dual(const DevCsr& k, const DevIter& it, bool seq, unsigned long long cond,
                  int use_cond, cudaStream_t s);
+// Separate step decision (it.decide_sep): sums the dual partials once.
+void launch_decide(const DevIter& it, cudaStream_t s, unsigned long long cond = 0, int use_cond = 0);
 // Primal side: K'y' + average + next trial x' (mode from state, or forced).
 void launch_primal(const DevCsr& kt, const DevIter& it, bool seq, int mode_override,
                    cudaStream_t s, unsigned long long cond = 0, int use_cond = 0);
@@ -56,12 +64,12 @@ void launch_restart_copy(const DevIter& it, int from_avg, cudaStream_t s);
 
 // ---- evaluation ------------------------------------------------------------
 void launch_eval(const DevCsr& k, const DevCsr& kt, const DevIter& it, const DevEval& ev,
-                 bool seq, cudaStream_t s);
+                 bool seq, cudaStream_t s, const PhaseFn& phase = {});
 int eval_grid0(int n, int m);
 int eval_grid(int ntiles);
 // Reduced costs of one evaluated point (slot 0..3) into lam[slot] (finish only).
 void launch_eval_lambda(const DevCsr& kt, const DevIter& it, const DevEval& ev, bool seq, int slot,
-                        cudaStream_t s);
+                        cudaStream_t s, const PhaseFn& phase = {});
 void launch_reduced_of_objective(const double* c, const double* l, const double* u, int n,
                                  double* lam, cudaStream_t s);
 

@@ -42,6 +42,16 @@ void validate_params(const pdlp_params& p) {  // SolverParams::validate, solver.
   if (p.pock_chambolle_alpha < 0.0 || p.pock_chambolle_alpha > 2.0)
     invalid("pock-chambolle: alpha must lie in [0, 2]");
   if (p.mode != PDLP_MODE_FAST && p.mode != PDLP_MODE_PARITY) invalid("params: unknown mode");
+  if (p.world_size < 1 || p.world_size > kMaxShards)
+    invalid("params: world_size must lie in [1, " + std::to_string(kMaxShards) + "]");
+  if (p.rank < 0 || p.rank >= p.world_size) invalid("params: rank must lie in [0, world_size)");
+  if (p.plan_world < 0 || p.plan_world > kMaxShards) invalid("params: plan_world out of range");
+  if (p.world_size > 1 && p.plan_world != 0 && p.plan_world != p.world_size)
+    invalid("params: plan_world must equal world_size on a sharded rank");
+  if (p.world_size > 1 && p.mode == PDLP_MODE_PARITY)
+    invalid("params: parity mode runs on one device (world_size 1)");
+  if (p.world_size > 1 && p.engine == PDLP_ENGINE_PERSISTENT)
+    invalid("params: the persistent engine runs on one device (world_size 1)");
 }
 
 // GeneralFormLp::validate (lp_model.hpp:45-72), then SolverParams::validate;
@@ -111,6 +121,7 @@ Solver::Solver(const pdlp_lp& lp, const pdlp_params& params) : params_(params) {
 }
 
 Solver::~Solver() {
+  for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
   if (ev_begin_) cudaEventDestroy(ev_begin_);
   if (ev_end_) cudaEventDestroy(ev_end_);
   if (ev_w0_) cudaEventDestroy(ev_w0_);
@@ -217,23 +228,63 @@ void Solver::setup(const pdlp_lp& lp) {
   PDLP_CUDA(cudaStreamSynchronize(s));
   K_ = DevCsr{k_rp_.get(), k_col_.get(), k_val_.get(), k_val_orig_.get(), int(m_), int(n_), nnz_};
   KT_ = DevCsr{kt_rp_.get(), kt_col_.get(), kt_val_.get(), kt_val_orig_.get(), int(n_), int(m_), nnz_};
+  // row sharding: contiguous row ranges of K and of K^T per rank (SURVEY.md
+  // §8e), cut where every tiling starts a tile, so each rank runs whole tiles
+  // of the one global plan and partials keep their global order
+  world_ = params_.world_size;
+  rank_ = params_.rank;
+  const int plan_world = params_.plan_world > 0 ? params_.plan_world : world_;
+  std::vector<int64_t> kbrk, ktbrk;
+  k_cuts_ = {0, m_};
+  kt_cuts_ = {0, n_};
+  if (plan_world > 1) {
+    const std::vector<int64_t> kc = shard_cuts<int>(m_, rp_h.data(), plan_world);
+    const std::vector<int64_t> ktc = shard_cuts<int>(n_, rpt_h.data(), plan_world);
+    kbrk.assign(kc.begin() + 1, kc.end() - 1);
+    ktbrk.assign(ktc.begin() + 1, ktc.end() - 1);
+    if (world_ > 1) {
+      k_cuts_ = kc;
+      kt_cuts_ = ktc;
+    }
+  }
+  const int64_t r0 = k_cuts_[rank_], r1 = k_cuts_[rank_ + 1];
+  const int64_t c0 = world_ > 1 ? kt_cuts_[rank_] : 0, c1 = world_ > 1 ? kt_cuts_[rank_ + 1] : n_;
   // three tilings of each operator: iteration kernels, persistent window
   // kernel, evaluation kernels (common.cuh TileGeom)
-  build_plan(k_it_, K_, rp_h, kIterGeom);
-  build_plan(kt_it_, KT_, rpt_h, kIterGeom);
-  build_plan(k_win_, K_, rp_h, kWinGeom);
-  build_plan(kt_win_, KT_, rpt_h, kWinGeom);
-  build_plan(k_ev_, K_, rp_h, kEvalGeom);
-  build_plan(kt_ev_, KT_, rpt_h, kEvalGeom);
+  build_plan(k_it_, K_, rp_h, kIterGeom, kbrk, r0, r1);
+  build_plan(kt_it_, KT_, rpt_h, kIterGeom, ktbrk, c0, c1);
+  build_plan(k_win_, K_, rp_h, kWinGeom, {}, 0, m_);
+  build_plan(kt_win_, KT_, rpt_h, kWinGeom, {}, 0, n_);
+  build_plan(k_ev_, K_, rp_h, kEvalGeom, kbrk, r0, r1);
+  build_plan(kt_ev_, KT_, rpt_h, kEvalGeom, ktbrk, c0, c1);
   K_ = k_it_.csr;
   KT_ = kt_it_.csr;
+  K_full_ = K_;
+  K_full_.tile0 = 0;
+  K_full_.ntiles = int(k_it_.plan.tiles.size());
+  KT_full_ = KT_;
+  KT_full_.tile0 = 0;
+  KT_full_.ntiles = int(kt_it_.plan.tiles.size());
+  if (world_ > 1) {
+    for (const OpPlan* op : {&k_it_, &kt_it_, &k_ev_, &kt_ev_})
+      if (op->csr.ntiles < 1) invalid("shards: a rank owns no tile; use fewer ranks for this instance");
+    // fingerprint of the partition: every rank must agree before linking
+    uint64_t h = 1469598103934665603ull;
+    auto mix = [&](uint64_t v) { h = (h ^ v) * 1099511628211ull; };
+    mix(uint64_t(n_)), mix(uint64_t(m_)), mix(uint64_t(nnz_)), mix(uint64_t(world_));
+    for (int64_t v : k_cuts_) mix(uint64_t(v));
+    for (int64_t v : kt_cuts_) mix(uint64_t(v));
+    for (const OpPlan* op : {&k_it_, &kt_it_, &k_ev_, &kt_ev_}) mix(op->plan.tiles.size());
+    plan_hash_ = h;
+  }
 
   allocate_iteration();
   set_kernel_attributes();
 }
 
 void Solver::build_plan(OpPlan& p, const DevCsr& base, const std::vector<int>& rp,
-                        const TileGeom& g) {
+                        const TileGeom& g, const std::vector<int64_t>& breaks, int64_t r0,
+                        int64_t r1) {
   // planner thresholds: env overrides are a tuning aid (clamped to the geometry)
   auto knob = [](const char* name, int def) {
     const char* v = std::getenv(name);
@@ -244,7 +295,7 @@ void Solver::build_plan(OpPlan& p, const DevCsr& base, const std::vector<int>& r
   const int cnnz = std::min(knob("PDLP_CHUNK_NNZ", g.chunk_nnz), g.chunk_nnz);
   const int lane = std::min(knob("PDLP_LANE_NNZ", g.lane_nnz), g.lane_nnz);
   p.plan = plan_tiles<int>(int64_t(rp.size()) - 1, rp.data(), parity(), smax, wmax, cnnz,
-                           g.stream_nnz, g.stream_rows, kThreads, lane);
+                           g.stream_nnz, g.stream_rows, kThreads, lane, breaks);
   const std::vector<Tile>& th = p.plan.tiles;
   p.tiles.alloc(th.size());
   PDLP_CUDA(cudaMemcpyAsync(p.tiles.get(), th.data(), th.size() * sizeof(Tile),
@@ -254,7 +305,9 @@ void Solver::build_plan(OpPlan& p, const DevCsr& base, const std::vector<int>& r
   p.ctr.zero(stream_);
   p.csr = base;
   p.csr.tiles = p.tiles.get();
-  p.csr.ntiles = int(th.size());
+  const auto own = tile_range(p.plan, r0, r1);  // this rank's tiles (all of them unsharded)
+  p.csr.tile0 = own.first;
+  p.csr.ntiles = own.second - own.first;
   p.csr.chunk_slots = p.plan.chunk_slots;
   p.csr.chunk_part = p.chunk.get();
   p.csr.chunk_ctr = p.ctr.get();
@@ -368,18 +421,21 @@ void Solver::precondition() {
 
 void Solver::allocate_iteration() {
   cudaStream_t s = stream_;
-  for (auto& b : x_) b.alloc(n_);
-  for (auto& b : y_) b.alloc(m_);
+  x_all_.alloc(3 * size_t(n_));
+  y_all_.alloc(3 * size_t(m_));
   for (auto& b : kx_) b.alloc(m_);
   for (auto& b : kty_) b.alloc(n_);
   avg_x_.alloc(n_);
   avg_y_.alloc(m_);
   x_start_.alloc(n_);
   y_start_.alloc(m_);
-  const int avg_blocks = std::max<int64_t>(1, (m_ + 4095) / 4096);
+  const int64_t row0 = k_cuts_[rank_], row1 = k_cuts_[rank_ + 1];
+  const int64_t col0 = kt_cuts_[rank_], col1 = kt_cuts_[rank_ + 1];
+  const int avg_blocks = std::max<int64_t>(1, (row1 - row0 + 4095) / 4096);
   const int p_grid = KT_.ntiles + avg_blocks;
-  d_part_.alloc(size_t(K_.ntiles) * 3);
-  p_part_.alloc(size_t(p_grid) * 4 + 2);  // two parity buffers
+  const int k_tiles = int(k_it_.plan.tiles.size()), kt_tiles = int(kt_it_.plan.tiles.size());
+  d_part_.alloc(size_t(k_tiles) * 3);
+  p_part_.alloc(size_t(kt_tiles) * 4 + 2);  // two parity buffers + dx^2 total
   p_part_.zero(s);
   const bool seq = parity();
   seq_dy2_.alloc(seq ? m_ : 1);
@@ -403,8 +459,8 @@ void Solver::allocate_iteration() {
 
   DevIter& it = it_;
   for (int i = 0; i < 3; ++i) {
-    it.x[i] = x_[i].get();
-    it.y[i] = y_[i].get();
+    it.x[i] = x_all_.get() + size_t(i) * n_;
+    it.y[i] = y_all_.get() + size_t(i) * m_;
   }
   for (int i = 0; i < 2; ++i) {
     it.kx[i] = kx_[i].get();
@@ -422,6 +478,7 @@ void Solver::allocate_iteration() {
   it.m = int(m_);
   it.m1 = int(m1_);
   it.p_grid = p_grid;
+  it.p_tiles = kt_tiles;
   {
     // l = +0 (sign bit clear, so l / d2 stays +0) and u = +inf everywhere:
     // min(max(v, l), u) == max(v, 0) bitwise, and the bound streams are skipped
@@ -433,9 +490,13 @@ void Solver::allocate_iteration() {
   it.avg_blocks = avg_blocks;
   it.d_part = d_part_.get();
   it.p_part = p_part_.get();
-  it.px_total = p_part_.get() + size_t(p_grid) * 4;
+  it.px_total = p_part_.get() + size_t(kt_tiles) * 4;
   it.snap = snap_dev_.get();
-  it.d_tiles = K_.ntiles;
+  it.d_tiles = k_tiles;
+  // per-CTA decisions re-read every dual partial: past ~2M partial reads per
+  // trial a one-CTA decision kernel is cheaper (C3/C4-sized operators)
+  it.decide_sep = (!parity() && double(k_tiles) * double(p_grid) > 2.0e6) ? 1 : 0;
+  if (const char* e = std::getenv("PDLP_DECIDE_SEP")) it.decide_sep = parity() ? 0 : std::atoi(e);
   it.seq_dy2 = seq_dy2_.get();
   it.seq_inter = seq_inter_.get();
   it.seq_dx2 = seq_dx2_.get();
@@ -466,8 +527,9 @@ void Solver::allocate_iteration() {
   scratch_n_.alloc(n_);
   const int grid0 = eval_grid0(int(n_), int(m_));
   part0_.alloc(size_t(std::max(1, grid0)) * 4);
-  part1_.alloc(size_t(eval_grid(k_ev_.csr.ntiles)) * 14);
-  part2_.alloc(size_t(eval_grid(kt_ev_.csr.ntiles)) * 18);
+  const int ev1_tiles = int(k_ev_.plan.tiles.size()), ev2_tiles = int(kt_ev_.plan.tiles.size());
+  part1_.alloc(size_t(ev1_tiles) * 14);
+  part2_.alloc(size_t(ev2_tiles) * 18);
   seq_r_.alloc(seq ? size_t(m_) * 4 : 1);
   seq_d_.alloc(seq ? size_t(n_) * 4 : 1);
   eval_dev_.alloc(1);
@@ -489,6 +551,43 @@ void Solver::allocate_iteration() {
   ev.seq_r = seq_r_.get();
   ev.seq_d = seq_d_.get();
   ev.out = eval_dev_.get();
+  ev.ev1_tiles = ev1_tiles;
+  ev.ev2_tiles = ev2_tiles;
+
+  // sharding: own slices, sync block, peer table (own entries until linked)
+  sync_.alloc(1);
+  sync_.zero(s);
+  shv_dev_.alloc(1);
+  it.world = world_, it.rank = rank_;
+  it.row0 = int(row0), it.row1 = int(row1), it.col0 = int(col0), it.col1 = int(col1);
+  it.sync = sync_.get();
+  it.shv = shv_dev_.get();
+  ev.world = world_, ev.rank = rank_;
+  ev.sync = sync_.get();
+  ev.shv = shv_dev_.get();
+  for (int q = 0; q < kMaxShards; ++q) {
+    shv_.x_all[q] = x_all_.get();
+    shv_.y_all[q] = y_all_.get();
+    shv_.d_part[q] = d_part_.get();
+    shv_.p_part[q] = p_part_.get();
+    shv_.avg_x[q] = avg_x_.get();
+    shv_.avg_y[q] = avg_y_.get();
+    shv_.part1[q] = part1_.get();
+    shv_.part2[q] = part2_.get();
+    shv_.lam[q] = lam_.get();
+    shv_.sync[q] = sync_.get();
+  }
+  shard_view_upload();
+  linked_ = world_ == 1;
+}
+
+void Solver::shard_view_upload() {
+  PDLP_CUDA(cudaMemcpyAsync(shv_dev_.get(), &shv_, sizeof(ShardView), cudaMemcpyHostToDevice, stream_));
+  PDLP_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void Solver::require_linked() const {
+  if (!linked_) throw std::logic_error("sharded rank: peers not linked (pdlp_shard_link_local / import)");
 }
 
 // The evaluation window as one CUDA graph: WHILE(cond) { dual; primal }, the
@@ -508,8 +607,10 @@ void Solver::capture_window_graph() {
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   PDLP_CUDA(cudaStreamBeginCaptureToGraph(stream_, body, nullptr, nullptr, 0,
                                           cudaStreamCaptureModeThreadLocal));
-  launch_dual(K_, it_, parity(), static_cast<unsigned long long>(h), 1, stream_);
-  launch_primal(KT_, it_, parity(), -1, stream_, static_cast<unsigned long long>(h), 1);
+  const unsigned long long ch = static_cast<unsigned long long>(h);
+  launch_dual(K_, it_, parity(), ch, it_.decide_sep ? 0 : 1, stream_);
+  if (it_.decide_sep) launch_decide(it_, stream_, ch, 1);
+  launch_primal(KT_, it_, parity(), -1, stream_, ch, it_.decide_sep ? 0 : 1);
   PDLP_CUDA(cudaStreamEndCapture(stream_, &body));
   PDLP_CUDA(cudaGraphInstantiate(&graph_exec_, graph_, 0));
   cond_handle_ = static_cast<unsigned long long>(h);
@@ -535,6 +636,8 @@ double Solver::elapsed() const {
 // ---------------------------------------------------------------------------
 
 void Solver::iterate_begin(int32_t* status) {
+  PDLP_CUDA(cudaSetDevice(params_.device));
+  require_linked();
   t0_ = std::chrono::steady_clock::now();
   DevState& st = *hs_.get();
   std::memset(&st, 0, sizeof st);
@@ -577,6 +680,7 @@ void Solver::iterate_begin(int32_t* status) {
     // first trial x' = proj(x - tau (c - K'y)) at z = 0
     upload_state();
     launch_primal(KT_, it_, parity(), kPRetry, stream_);
+    phase();
     ++launches_;
     p_from_window_ = false;
   }
@@ -585,6 +689,7 @@ void Solver::iterate_begin(int32_t* status) {
 
 void Solver::iterate_run(int64_t count, int32_t* status) {
   if (!begun_ || !state_valid_) throw std::logic_error("iterate_run before iterate_begin");
+  PDLP_CUDA(cudaSetDevice(params_.device));
   DevState& st = *hs_.get();
   const int64_t freq = params_.evaluation_frequency;
   int64_t done = 0;
@@ -646,8 +751,8 @@ void Solver::run_window(int target) {
   if (engine_ == PDLP_ENGINE_PERSISTENT) {
     WinBufs wb = wb_;
     wb.p_src = p_from_window_ ? wb_.wp_part
-                              : it_.p_part + size_t(st.trials_total & 1) * it_.p_grid * 2;
-    wb.p_src_count = p_from_window_ ? win_grid_ : it_.p_grid;
+                              : it_.p_part + size_t(st.trials_total & 1) * it_.p_tiles * 2;
+    wb.p_src_count = p_from_window_ ? win_grid_ : it_.p_tiles;
     launch_window(k_win_.csr, kt_win_.csr, it_, wb, win_grid_, stream_);
     p_from_window_ = true;
     launches_ += 1;
@@ -659,7 +764,10 @@ void Solver::run_window(int target) {
     while (true) {
       for (int i = 0; i < remaining; ++i) {
         launch_dual(K_, it_, parity(), 0, 0, stream_);
+        phase();
+        if (it_.decide_sep) launch_decide(it_, stream_);
         launch_primal(KT_, it_, parity(), -1, stream_);
+        phase();
       }
       download_state();
       if (st.failure || st.window_accepts >= target) break;
@@ -669,7 +777,7 @@ void Solver::run_window(int target) {
   PDLP_CUDA(cudaEventRecord(ev_w1_, stream_));
   // the evaluation block is enqueued behind the window (it reads the device
   // state), so one host round trip per window brings back state, scalars, log
-  launch_eval(k_ev_.csr, kt_ev_.csr, it_, ev_, parity(), stream_);
+  launch_eval(k_ev_.csr, kt_ev_.csr, it_, ev_, parity(), stream_, phase_);
   launches_ += parity() ? 5 : 4;
   ++evaluations_;
   PDLP_CUDA(cudaMemcpyAsync(hs_.get(), state_dev_.get(), sizeof(DevState), cudaMemcpyDeviceToHost,
@@ -687,7 +795,8 @@ void Solver::run_window(int target) {
     PDLP_CUDA(cudaEventElapsedTime(&ms, ev_w0_, ev_w1_));
     window_seconds_ += 1e-3 * double(ms);
   }
-  if (engine_ != PDLP_ENGINE_PERSISTENT) launches_ += 2 * (st.trials_total - trials_before);
+  if (engine_ != PDLP_ENGINE_PERSISTENT)
+    launches_ += (it_.decide_sep ? 3 : 2) * (st.trials_total - trials_before);
   if (st.record_log && st.window_accepts > 0)
     step_log_.insert(step_log_.end(), log_host_.get(), log_host_.get() + st.window_accepts);
 }
@@ -695,7 +804,7 @@ void Solver::run_window(int target) {
 void Solver::evaluate() {
   if (eval_fresh_) return;  // nothing changed since the window's own evaluation
   upload_state();
-  launch_eval(k_ev_.csr, kt_ev_.csr, it_, ev_, parity(), stream_);
+  launch_eval(k_ev_.csr, kt_ev_.csr, it_, ev_, parity(), stream_, phase_);
   launches_ += parity() ? 5 : 4;
   ++evaluations_;
   PDLP_CUDA(cudaMemcpyAsync(he_.get(), eval_dev_.get(), sizeof(EvalOut), cudaMemcpyDeviceToHost,
@@ -794,6 +903,7 @@ void Solver::evaluation_block() {
   upload_state();
   launch_spmv(K_, false, it_.x[st.ix_cur], it_.kx[st.ikx_cur], parity(), stream_);
   launch_primal(KT_, it_, parity(), kPRestart, stream_);
+  phase();
   launches_ += 3;
   eval_fresh_ = false;
   p_from_window_ = false;
@@ -828,7 +938,7 @@ void Solver::finish(int status, int slot_x, int slot_y, int slot_lam, const KktH
                                 sizeof(double), m_, cudaMemcpyDeviceToHost, s));
   if (n_) {
     if (slot_lam >= 0) {
-      launch_eval_lambda(kt_ev_.csr, it_, ev_, parity(), slot_lam, s);
+      launch_eval_lambda(kt_ev_.csr, it_, ev_, parity(), slot_lam, s, phase_);
       PDLP_CUDA(cudaMemcpyAsync(rlam_.data(), lam_.get() + size_t(slot_lam) * n_,
                                 n_ * sizeof(double), cudaMemcpyDeviceToHost, s));
     } else {
@@ -892,8 +1002,8 @@ void Solver::get_iterate(double* x, double* y, double* kx, double* kty, int64_t*
   if (!state_valid_) throw std::logic_error("no live iterate (call iterate_begin)");
   const DevState& st = *hs_.get();
   cudaStream_t s = stream_;
-  if (x && n_) PDLP_CUDA(cudaMemcpyAsync(x, x_[st.ix_cur].get(), n_ * 8, cudaMemcpyDeviceToHost, s));
-  if (y && m_) PDLP_CUDA(cudaMemcpyAsync(y, y_[st.iy_cur].get(), m_ * 8, cudaMemcpyDeviceToHost, s));
+  if (x && n_) PDLP_CUDA(cudaMemcpyAsync(x, it_.x[st.ix_cur], n_ * 8, cudaMemcpyDeviceToHost, s));
+  if (y && m_) PDLP_CUDA(cudaMemcpyAsync(y, it_.y[st.iy_cur], m_ * 8, cudaMemcpyDeviceToHost, s));
   if (kx && m_)
     PDLP_CUDA(cudaMemcpyAsync(kx, kx_[st.ikx_cur].get(), m_ * 8, cudaMemcpyDeviceToHost, s));
   if (kty && n_)
@@ -950,7 +1060,7 @@ void Solver::spmv(int op, const double* in, double* out) {
   const int64_t nin = transpose ? m_ : n_, nout = transpose ? n_ : m_;
   DevBuf<double> din(nin), dout(nout);
   if (nin) PDLP_CUDA(cudaMemcpyAsync(din.get(), in, nin * 8, cudaMemcpyHostToDevice, stream_));
-  launch_spmv(transpose ? KT_ : K_, orig, din.get(), dout.get(), parity(), stream_);
+  launch_spmv(transpose ? KT_full_ : K_full_, orig, din.get(), dout.get(), parity(), stream_);
   if (nout) PDLP_CUDA(cudaMemcpyAsync(out, dout.get(), nout * 8, cudaMemcpyDeviceToHost, stream_));
   PDLP_CUDA(cudaStreamSynchronize(stream_));
 }
@@ -959,6 +1069,7 @@ void Solver::spmv(int op, const double* in, double* out) {
 // repetition runs a real trial (dual then primal); the events bracket only the
 // kernel being timed. Leaves the iterate state invalid.
 void Solver::time_kernel(int which, int reps, double* avg_ms, double* bytes) {
+  if (world_ > 1) throw std::logic_error("time_kernel: single-device handles only");
   if (!begun_) {
     int32_t s;
     iterate_begin(&s);
@@ -1015,6 +1126,7 @@ void Solver::time_kernel(int which, int reps, double* avg_ms, double* bytes) {
   for (int r = 0; r < reps; ++r) {
     if (which == 0) PDLP_CUDA(cudaEventRecord(ev[2 * r], stream_));
     launch_dual(K_, it_, parity(), 0, 0, stream_);
+    if (it_.decide_sep) launch_decide(it_, stream_);
     if (which == 0) PDLP_CUDA(cudaEventRecord(ev[2 * r + 1], stream_));
     if (which == 1) PDLP_CUDA(cudaEventRecord(ev[2 * r], stream_));
     launch_primal(KT_, it_, parity(), -1, stream_);
@@ -1047,6 +1159,140 @@ void Solver::sizes(int64_t* out) const {
   out[1] = m_;
   out[2] = m1_;
   out[3] = nnz_;
+}
+
+// ---------------------------------------------------------------------------
+// sharding: linking the ranks
+// ---------------------------------------------------------------------------
+
+LocalGroup::LocalGroup(int world) : world_(world), ev_(size_t(world), nullptr) {
+  for (auto& e : ev_) PDLP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+}
+
+LocalGroup::~LocalGroup() {
+  for (auto& e : ev_)
+    if (e) cudaEventDestroy(e);
+}
+
+void LocalGroup::barrier() {
+  std::unique_lock<std::mutex> lk(mu_);
+  const unsigned long long gen = gen_;
+  if (++arrived_ == world_) {
+    arrived_ = 0;
+    ++gen_;
+    cv_.notify_all();
+    return;
+  }
+  if (!cv_.wait_for(lk, std::chrono::seconds(120), [&] { return gen_ != gen; }))
+    throw std::runtime_error("shard group: a rank did not reach the barrier within 120 s");
+}
+
+void LocalGroup::phase(int rank, cudaStream_t s) {
+  PDLP_CUDA(cudaEventRecord(ev_[size_t(rank)], s));
+  barrier();
+  for (int q = 0; q < world_; ++q)
+    if (q != rank) PDLP_CUDA(cudaStreamWaitEvent(s, ev_[size_t(q)], 0));
+  barrier();  // nobody records its next event before every peer enqueued its waits
+}
+
+void Solver::link_local(const std::vector<Solver*>& ranks) {
+  const int world = int(ranks.size());
+  if (world < 2) invalid("shard link: need at least two ranks");
+  for (int q = 0; q < world; ++q) {
+    const Solver* r = ranks[size_t(q)];
+    if (!r) invalid("shard link: null handle");
+    if (r->world_ != world || r->rank_ != q) invalid("shard link: handles must be ranks 0..world-1 in order");
+    if (r->plan_hash_ != ranks[0]->plan_hash_) invalid("shard link: ranks were built from different instances");
+  }
+  auto group = std::make_shared<LocalGroup>(world);
+  ShardView v{};
+  for (int q = 0; q < world; ++q) {
+    const Solver* r = ranks[size_t(q)];
+    v.x_all[q] = r->x_all_.get();
+    v.y_all[q] = r->y_all_.get();
+    v.d_part[q] = r->d_part_.get();
+    v.p_part[q] = r->p_part_.get();
+    v.avg_x[q] = r->avg_x_.get();
+    v.avg_y[q] = r->avg_y_.get();
+    v.part1[q] = r->part1_.get();
+    v.part2[q] = r->part2_.get();
+    v.lam[q] = r->lam_.get();
+    v.sync[q] = r->sync_.get();
+  }
+  for (int q = 0; q < world; ++q) {
+    Solver* r = ranks[size_t(q)];
+    PDLP_CUDA(cudaSetDevice(r->params_.device));
+    r->shv_ = v;
+    r->shard_view_upload();
+    r->group_ = group;
+    cudaStream_t st = r->stream_;
+    LocalGroup* g = group.get();
+    r->phase_ = [g, q, st] { g->phase(q, st); };
+    // host-ordered launches: the per-launch phases need the stream engine
+    r->engine_ = PDLP_ENGINE_STREAM;
+    r->linked_ = true;
+  }
+}
+
+void Solver::export_shard(ShardBlob* out) const {
+  if (world_ < 2) invalid("shard export: not a sharded handle (world_size 1)");
+  ShardBlob b{};
+  b.magic = 0x50444c50u;  // "PDLP"
+  b.rank = rank_;
+  b.world = world_;
+  b.device = params_.device;
+  b.n = n_, b.m = m_, b.nnz = nnz_;
+  b.plan_hash = plan_hash_;
+  const void* bufs[10] = {x_all_.get(), y_all_.get(), d_part_.get(), p_part_.get(), avg_x_.get(),
+                          avg_y_.get(), part1_.get(), part2_.get(), lam_.get(), sync_.get()};
+  PDLP_CUDA(cudaSetDevice(params_.device));
+  for (int i = 0; i < 10; ++i) PDLP_CUDA(cudaIpcGetMemHandle(&b.h[i], const_cast<void*>(bufs[i])));
+  *out = b;
+}
+
+void Solver::import_shards(const ShardBlob* blobs, int world) {
+  if (world != world_) invalid("shard import: world size differs from this handle's");
+  PDLP_CUDA(cudaSetDevice(params_.device));
+  ShardView v = shv_;
+  for (int q = 0; q < world; ++q) {
+    const ShardBlob& b = blobs[q];
+    if (b.magic != 0x50444c50u || b.rank != q || b.world != world)
+      invalid("shard import: blobs must be every rank's export, in rank order");
+    if (b.plan_hash != plan_hash_ || b.n != n_ || b.m != m_ || b.nnz != nnz_)
+      invalid("shard import: ranks were built from different instances or partitions");
+    if (q == rank_) continue;
+    void* p[10];
+    for (int i = 0; i < 10; ++i) {
+      PDLP_CUDA(cudaIpcOpenMemHandle(&p[i], b.h[i], cudaIpcMemLazyEnablePeerAccess));
+      ipc_opened_.push_back(p[i]);
+    }
+    v.x_all[q] = static_cast<double*>(p[0]);
+    v.y_all[q] = static_cast<double*>(p[1]);
+    v.d_part[q] = static_cast<double*>(p[2]);
+    v.p_part[q] = static_cast<double*>(p[3]);
+    v.avg_x[q] = static_cast<double*>(p[4]);
+    v.avg_y[q] = static_cast<double*>(p[5]);
+    v.part1[q] = static_cast<double*>(p[6]);
+    v.part2[q] = static_cast<double*>(p[7]);
+    v.lam[q] = static_cast<double*>(p[8]);
+    v.sync[q] = static_cast<ShardSync*>(p[9]);
+  }
+  shv_ = v;
+  shard_view_upload();
+  linked_ = true;  // in-kernel flag barriers order the ranks (any engine but persistent)
+}
+
+void Solver::shard_info(int64_t* out) const {
+  out[0] = world_;
+  out[1] = rank_;
+  out[2] = k_cuts_[size_t(rank_)];
+  out[3] = k_cuts_[size_t(rank_) + 1];
+  out[4] = kt_cuts_[size_t(rank_)];
+  out[5] = kt_cuts_[size_t(rank_) + 1];
+  out[6] = K_.ntiles;
+  out[7] = KT_.ntiles;
+  out[8] = int64_t(k_it_.plan.tiles.size());
+  out[9] = int64_t(kt_it_.plan.tiles.size());
 }
 
 }  // namespace pdlp

@@ -4,12 +4,16 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <condition_variable>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
 #include "../../include/pdlp_b200.h"
 #include "common.cuh"
 #include "device_state.h"
+#include "kernels.cuh"
 #include "tiles.h"
 #include "window.cuh"
 
@@ -80,6 +84,38 @@ struct KktHost {  // KktResiduals (solver.hpp:109-123)
   double weighted(double omega) const;
 };
 
+// Ranks of one sharded solve living in ONE process (the loopback transport:
+// every rank on its own stream, usually the same device). After each launch
+// whose outputs peers consume, every rank records an event, meets the others
+// at a host barrier and makes its stream wait on every peer's event, so no
+// consumer kernel ever starts (and spins) before its producers finished.
+class LocalGroup {
+ public:
+  explicit LocalGroup(int world);
+  ~LocalGroup();
+  void phase(int rank, cudaStream_t s);
+  int world() const { return world_; }
+
+ private:
+  void barrier();
+  int world_;
+  std::vector<cudaEvent_t> ev_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  int arrived_ = 0;
+  unsigned long long gen_ = 0;
+};
+
+// Exported view of one rank's exchanged buffers (CUDA IPC handles).
+struct ShardBlob {
+  uint32_t magic;
+  int32_t rank, world;
+  int32_t device;
+  int64_t n, m, nnz;
+  uint64_t plan_hash;
+  cudaIpcMemHandle_t h[10];  // x_all y_all d_part p_part avg_x avg_y part1 part2 lam sync
+};
+
 class Solver {
  public:
   Solver(const pdlp_lp& lp, const pdlp_params& params);
@@ -97,6 +133,11 @@ class Solver {
   void spmv(int op, const double* in, double* out);
   void time_kernel(int which, int reps, double* avg_ms, double* bytes);
   void sizes(int64_t* out) const;
+  // ---- sharding ----
+  static void link_local(const std::vector<Solver*>& ranks);
+  void export_shard(ShardBlob* out) const;
+  void import_shards(const ShardBlob* blobs, int world);
+  void shard_info(int64_t* out) const;
   const pdlp_result_info& info() const { return info_; }
 
  private:
@@ -110,7 +151,13 @@ class Solver {
     DevBuf<unsigned> ctr;
     DevCsr csr{};
   };
-  void build_plan(OpPlan& p, const DevCsr& base, const std::vector<int>& rp, const TileGeom& g);
+  void build_plan(OpPlan& p, const DevCsr& base, const std::vector<int>& rp, const TileGeom& g,
+                  const std::vector<int64_t>& breaks, int64_t r0, int64_t r1);
+  void shard_view_upload();
+  void phase() {
+    if (phase_) phase_();
+  }
+  void require_linked() const;
   void allocate_iteration();
   void capture_window_graph();
   void upload_state();
@@ -140,12 +187,14 @@ class Solver {
   DevBuf<int> k_rp_, k_col_, kt_rp_, kt_col_;
   DevBuf<double> k_val_, k_val_orig_, kt_val_, kt_val_orig_;
   OpPlan k_it_, kt_it_, k_win_, kt_win_, k_ev_, kt_ev_;
-  DevCsr K_{}, KT_{};  // the iteration-kernel tilings
+  DevCsr K_{}, KT_{};  // the iteration-kernel tilings (this rank's tiles)
+  DevCsr K_full_{}, KT_full_{};  // every tile (kernel-level API on a sharded rank)
 
   // vectors
   DevBuf<double> c_orig_, l_orig_, u_orig_, q_orig_, d1_dev_, d2_dev_;
   DevBuf<double> c_s_, l_s_, u_s_, q_s_;
-  DevBuf<double> x_[3], y_[3], kx_[2], kty_[2], avg_x_, avg_y_, x_start_, y_start_;
+  DevBuf<double> x_all_, y_all_;  // the three x (3 n) and y (3 m) rotation buffers
+  DevBuf<double> kx_[2], kty_[2], avg_x_, avg_y_, x_start_, y_start_;
   DevBuf<double> d_part_, p_part_, seq_dy2_, seq_inter_, seq_dx2_;
   DevBuf<double> red_tab_, gro_tab_;
   DevBuf<pdlp_step_log_entry> step_log_dev_;
@@ -186,6 +235,18 @@ class Solver {
   std::vector<pdlp_restart_event> restart_log_;
   pdlp_result_info info_{};
   std::vector<double> rx_, ry_, rlam_;
+
+  // ---- sharding (world_ == 1: a single device) ----
+  int world_ = 1, rank_ = 0;
+  std::vector<int64_t> k_cuts_, kt_cuts_;  // world + 1 row boundaries of K and K^T
+  uint64_t plan_hash_ = 0;
+  DevBuf<ShardSync> sync_;
+  DevBuf<ShardView> shv_dev_;
+  ShardView shv_{};
+  bool linked_ = false;
+  std::shared_ptr<LocalGroup> group_;
+  PhaseFn phase_;
+  std::vector<void*> ipc_opened_;
 };
 
 }  // namespace pdlp

@@ -1,5 +1,7 @@
 // tiles.cu — host-side tile planner (see tiles.h).
 #include <algorithm>
+#include <stdexcept>
+#include <string>
 
 #include "tiles.h"
 
@@ -8,20 +10,23 @@ namespace pdlp {
 template <class Off>
 TilePlan plan_tiles(int64_t rows, const Off* rp, bool parity, int stream_max_row,
                     int warp_max_row, int chunk_nnz, int stream_nnz, int stream_rows, int threads,
-                    int lane_nnz) {
+                    int lane_nnz, const std::vector<int64_t>& breaks) {
   TilePlan plan;
   int64_t r = 0;
+  size_t bi = 0;
   auto len = [&](int64_t i) { return int64_t(rp[i + 1] - rp[i]); };
   while (r < rows) {
+    while (bi < breaks.size() && breaks[bi] <= r) ++bi;
+    const int64_t brk = bi < breaks.size() ? breaks[bi] : rows;  // next forced tile start
     const int64_t l = len(r);
     if (l <= stream_max_row) {
       const int64_t r0 = r, k0 = rp[r];
-      while (r < rows && r - r0 < stream_rows && len(r) <= stream_max_row &&
+      while (r < brk && r - r0 < stream_rows && len(r) <= stream_max_row &&
              int64_t(rp[r + 1]) - k0 <= stream_nnz)
         ++r;
       // end interior tiles on a multiple of 4 rows so the 4-row groups of the
       // next tile stay 32-byte aligned for vector epilogues
-      if (r < rows && r - r0 > 4 && (r & 3) && len(r) <= stream_max_row) r -= (r & 3);
+      if (r < brk && r - r0 > 4 && (r & 3) && len(r) <= stream_max_row) r -= (r & 3);
       plan.tiles.push_back({kTileStream, int32_t(r0), int32_t(r), int32_t(k0), int32_t(rp[r]), 0, 1, 0});
       ++plan.stream_tiles;
     } else if (!parity && l <= warp_max_row) {
@@ -33,7 +38,7 @@ TilePlan plan_tiles(int64_t rows, const Off* rp, bool parity, int stream_max_row
       };
       const int g = lanes(l);
       const int64_t r0 = r;
-      while (r < rows && r - r0 < threads / g && len(r) > stream_max_row && len(r) <= warp_max_row &&
+      while (r < brk && r - r0 < threads / g && len(r) > stream_max_row && len(r) <= warp_max_row &&
              lanes(len(r)) == g)
         ++r;
       plan.tiles.push_back({kTileWarp, int32_t(r0), int32_t(r), int32_t(rp[r0]), int32_t(rp[r]), g, 1, 0});
@@ -62,8 +67,49 @@ TilePlan plan_tiles(int64_t rows, const Off* rp, bool parity, int stream_max_row
   return plan;
 }
 
-template TilePlan plan_tiles<int>(int64_t, const int*, bool, int, int, int, int, int, int, int);
+template <class Off>
+std::vector<int64_t> shard_cuts(int64_t rows, const Off* rp, int world) {
+  if (world < 1) throw std::invalid_argument("shards: world size must be >= 1");
+  std::vector<int64_t> cuts(size_t(world) + 1, 0);
+  cuts[size_t(world)] = rows;
+  const double total = double(rp[rows]) + double(rows);  // nnz + row work
+  int64_t r = 0;
+  for (int p = 1; p < world; ++p) {
+    const double target = total * double(p) / double(world);
+    // first row whose prefix weight reaches the target (binary search)
+    int64_t lo = r, hi = rows;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      if (double(rp[mid]) + double(mid) < target)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    int64_t c = lo & ~int64_t(3);
+    if (c <= cuts[size_t(p) - 1]) c = cuts[size_t(p) - 1] + 4;
+    if (c >= rows)
+      throw std::invalid_argument("shards: " + std::to_string(rows) + " rows cannot be split " +
+                                  std::to_string(world) + " ways");
+    cuts[size_t(p)] = c;
+    r = c;
+  }
+  return cuts;
+}
+
+std::pair<int, int> tile_range(const TilePlan& plan, int64_t r0, int64_t r1) {
+  int a = 0;
+  const int n = int(plan.tiles.size());
+  while (a < n && plan.tiles[size_t(a)].row0 < r0) ++a;
+  int b = a;
+  while (b < n && plan.tiles[size_t(b)].row0 < r1) ++b;
+  return {a, b};
+}
+
+template TilePlan plan_tiles<int>(int64_t, const int*, bool, int, int, int, int, int, int, int,
+                                  const std::vector<int64_t>&);
 template TilePlan plan_tiles<int64_t>(int64_t, const int64_t*, bool, int, int, int, int, int, int,
-                                      int);
+                                      int, const std::vector<int64_t>&);
+template std::vector<int64_t> shard_cuts<int>(int64_t, const int*, int);
+template std::vector<int64_t> shard_cuts<int64_t>(int64_t, const int64_t*, int);
 
 }  // namespace pdlp

@@ -17,6 +17,7 @@
 
 #include <stdint.h>
 
+#include <utility>
 #include <vector>
 
 namespace pdlp {
@@ -43,10 +44,21 @@ struct TilePlan {
 };
 
 // Builds the tile list for a CSR with `rows` rows and offsets `rp` (rows+1).
-// `parity` disables WARP tiles and row splitting.
+// `parity` disables WARP tiles and row splitting. `breaks` (sorted, may be
+// empty) are rows where a tile must start: the shard boundaries, so every
+// rank's rows are a contiguous run of whole tiles of the one global plan.
 template <class Off>
 TilePlan plan_tiles(int64_t rows, const Off* rp, bool parity, int stream_max_row,
                     int warp_max_row, int chunk_nnz, int stream_nnz, int stream_rows, int threads,
-                    int lane_nnz);
+                    int lane_nnz, const std::vector<int64_t>& breaks = {});
+
+// Shard boundaries: world + 1 rows 0 = c_0 < c_1 < ... < c_world = rows,
+// balancing nnz + rows per shard, interior cuts on multiples of 4 rows.
+// Throws std::invalid_argument when the operator is too small to split.
+template <class Off>
+std::vector<int64_t> shard_cuts(int64_t rows, const Off* rp, int world);
+
+// [first, last) indices of the tiles whose first row lies in [r0, r1).
+std::pair<int, int> tile_range(const TilePlan& plan, int64_t r0, int64_t r1);
 
 }  // namespace pdlp

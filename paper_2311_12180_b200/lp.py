@@ -233,7 +233,11 @@ class SolverParams:
     mode: Mode = Mode.FAST
     use_cuda_graph: bool = True
     l2_persist: bool = True
-    engine: int = 0  # abi.ENGINE_*: AUTO picks the persistent window kernel in fast mode
+    engine: int = 0  # abi.ENGINE_*: AUTO = the CUDA-graph window (STREAM without graphs)
+    # row sharding: rank `rank` of `world_size` (see ShardGroup)
+    world_size: int = 1
+    rank: int = 0
+    plan_world: int = 0  # tile breaks of a plan_world-way partition on one rank (verification)
 
     def validate(self) -> None:
         """SolverParams::validate (solver.hpp:79-93)."""

@@ -21,7 +21,7 @@ HEADER = ROOT / "include" / "pdlp_b200.h"
 
 def declared_symbols() -> list[str]:
     text = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
-    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*)\s+(pdlp_\w+)\s*\(", text, flags=re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|void|const char\*|const pdlp_lp\*)\s+(pdlp_\w+)\s*\(", text, flags=re.M)))
 
 
 def test_library_exports_every_declared_symbol():
