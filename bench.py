@@ -248,14 +248,22 @@ def run_ours(args):
     e2e_iters, e2e_s = 0, 0.0
     h2d = lp_bytes(lp)
     d2h = 8 * (2 * lp.num_variables + lp.num_constraints)  # x, y, lambda
+    parts = {"create_ms": 0.0, "solve_ms": 0.0, "destroy_ms": 0.0}
     for _ in range(max(1, args.steps)):
         flush.fill_(1.0)
         barrier()
         t0 = time.perf_counter()
-        with Solver(lp, params) as s2:  # pdlp_create: H2D + K^T + preconditioning
-            r2 = s2.solve()  # pdlp_solve + pdlp_get_solution (D2H)
+        s2 = Solver(lp, params)  # pdlp_create: H2D + K^T + preconditioning
+        t1 = time.perf_counter()
+        r2 = s2.solve()  # pdlp_solve + pdlp_get_solution (D2H)
+        t2 = time.perf_counter()
+        s2.close()
         torch.cuda.synchronize()
-        e2e_s += time.perf_counter() - t0
+        t3 = time.perf_counter()
+        e2e_s += t3 - t0
+        parts["create_ms"] += 1e3 * (t1 - t0) / args.steps
+        parts["solve_ms"] += 1e3 * (t2 - t1) / args.steps
+        parts["destroy_ms"] += 1e3 * (t3 - t2) / args.steps
         e2e_iters += r2.iterations
     et = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{device}")
     ei = torch.tensor([float(e2e_iters)], dtype=torch.float64, device=f"cuda:{device}")
@@ -278,7 +286,8 @@ def run_ours(args):
             "config": {"workload": WORKLOAD, "eps": 1e-4, "seed": generators.SEEDS["C2"],
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
                        "l2": "flushed between timed solves (256 MiB write); working set ~130 MB"},
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "per_step": parts},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": profile_traffic(), "peak_source": peak_kind,
                          "bytes_per_launch": by, "launch_us": 1e3 * ms},
@@ -287,6 +296,7 @@ def run_ours(args):
                                    "frac": b_iter(n, m, nnz) * value / world / 1e9 / peak},
             "kernels_us": {"dual": 1e3 * dual_ms, "primal": 1e3 * prim_ms},
             "time_to_tolerance_ms": 1e3 * last.info["device_seconds"], "iterations": last.iterations,
+            "window_ms": 1e3 * last.info["window_seconds"], "eval_ms": 1e3 * last.info["eval_seconds"],
             "restarts": last.restarts, "status": str(last.status),
             "primal_objective": last.info["primal_objective"],
             "setup_ms": 1e3 * last.info["setup_seconds"],

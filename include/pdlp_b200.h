@@ -194,6 +194,7 @@ typedef struct {
   int64_t trials;        /* total line-search trials (B200 extension) */
   int64_t evaluations;   /* evaluation blocks run (B200 extension) */
   int64_t gpu_launches;  /* kernels launched by the solve loop (B200 extension) */
+  double eval_seconds;   /* time inside the evaluation kernels, CUDA events (B200 extension) */
   char message[256];
 } pdlp_result_info;
 

@@ -118,6 +118,7 @@ class PdlpResultInfo(C.Structure):
         ("trials", C.c_int64),
         ("evaluations", C.c_int64),
         ("gpu_launches", C.c_int64),
+        ("eval_seconds", C.c_double),
         ("message", C.c_char * 256),
     ]
 

@@ -126,6 +126,7 @@ Solver::~Solver() {
   if (ev_end_) cudaEventDestroy(ev_end_);
   if (ev_w0_) cudaEventDestroy(ev_w0_);
   if (ev_w1_) cudaEventDestroy(ev_w1_);
+  if (ev_e1_) cudaEventDestroy(ev_e1_);
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
   if (graph_) cudaGraphDestroy(graph_);
   if (stream_) cudaStreamDestroy(stream_);
@@ -305,7 +306,7 @@ void Solver::build_plan(OpPlan& p, const DevCsr& base, const std::vector<int>& r
   p.ctr.zero(stream_);
   p.csr = base;
   p.csr.tiles = p.tiles.get();
-  const auto own = tile_range(p.plan, r0, r1);  // this rank's tiles (all of them unsharded)
+  const auto own = tile_range(p.plan, r0, r1, int64_t(rp.size()) - 1);  // this rank's tiles (all of them unsharded)
   p.csr.tile0 = own.first;
   p.csr.ntiles = own.second - own.first;
   p.csr.chunk_slots = p.plan.chunk_slots;
@@ -662,8 +663,10 @@ void Solver::iterate_begin(int32_t* status) {
     PDLP_CUDA(cudaEventCreate(&ev_end_));
     PDLP_CUDA(cudaEventCreate(&ev_w0_));
     PDLP_CUDA(cudaEventCreate(&ev_w1_));
+    PDLP_CUDA(cudaEventCreate(&ev_e1_));
   }
   window_seconds_ = 0.0;
+  eval_seconds_ = 0.0;
   PDLP_CUDA(cudaEventRecord(ev_begin_, stream_));
   upload_state();
   eval_fresh_ = false;
@@ -778,6 +781,7 @@ void Solver::run_window(int target) {
   // the evaluation block is enqueued behind the window (it reads the device
   // state), so one host round trip per window brings back state, scalars, log
   launch_eval(k_ev_.csr, kt_ev_.csr, it_, ev_, parity(), stream_, phase_);
+  PDLP_CUDA(cudaEventRecord(ev_e1_, stream_));
   launches_ += parity() ? 5 : 4;
   ++evaluations_;
   PDLP_CUDA(cudaMemcpyAsync(hs_.get(), state_dev_.get(), sizeof(DevState), cudaMemcpyDeviceToHost,
@@ -794,6 +798,8 @@ void Solver::run_window(int target) {
     float ms = 0.f;
     PDLP_CUDA(cudaEventElapsedTime(&ms, ev_w0_, ev_w1_));
     window_seconds_ += 1e-3 * double(ms);
+    PDLP_CUDA(cudaEventElapsedTime(&ms, ev_w1_, ev_e1_));
+    eval_seconds_ += 1e-3 * double(ms);
   }
   if (engine_ != PDLP_ENGINE_PERSISTENT)
     launches_ += (it_.decide_sep ? 3 : 2) * (st.trials_total - trials_before);
@@ -974,6 +980,7 @@ void Solver::finish(int status, int slot_x, int slot_y, int slot_lam, const KktH
     PDLP_CUDA(cudaEventElapsedTime(&ms, ev_begin_, ev_end_));
     in.device_seconds = 1e-3 * double(ms);
     in.window_seconds = window_seconds_;
+    in.eval_seconds = eval_seconds_;
   }
   in.step_log_size = int64_t(step_log_.size());
   in.restart_log_size = int64_t(restart_log_.size());

@@ -222,7 +222,8 @@ class Solver {
   int64_t launches_ = 0, evaluations_ = 0;
   double setup_seconds_ = 0.0;
   cudaEvent_t ev_begin_ = nullptr, ev_end_ = nullptr, ev_w0_ = nullptr, ev_w1_ = nullptr;
-  double window_seconds_ = 0.0;
+  double window_seconds_ = 0.0, eval_seconds_ = 0.0;
+  cudaEvent_t ev_e1_ = nullptr;
   // persistent window engine
   int engine_ = PDLP_ENGINE_PERSISTENT;
   int win_grid_ = 0;

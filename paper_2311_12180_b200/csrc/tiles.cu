@@ -96,12 +96,13 @@ std::vector<int64_t> shard_cuts(int64_t rows, const Off* rp, int world) {
   return cuts;
 }
 
-std::pair<int, int> tile_range(const TilePlan& plan, int64_t r0, int64_t r1) {
+std::pair<int, int> tile_range(const TilePlan& plan, int64_t r0, int64_t r1, int64_t rows) {
+  // the last shard also takes the empty tile of an operator without rows
   int a = 0;
   const int n = int(plan.tiles.size());
   while (a < n && plan.tiles[size_t(a)].row0 < r0) ++a;
   int b = a;
-  while (b < n && plan.tiles[size_t(b)].row0 < r1) ++b;
+  while (b < n && (r1 >= rows || plan.tiles[size_t(b)].row0 < r1)) ++b;
   return {a, b};
 }
 

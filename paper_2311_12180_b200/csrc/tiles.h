@@ -58,7 +58,8 @@ TilePlan plan_tiles(int64_t rows, const Off* rp, bool parity, int stream_max_row
 template <class Off>
 std::vector<int64_t> shard_cuts(int64_t rows, const Off* rp, int world);
 
-// [first, last) indices of the tiles whose first row lies in [r0, r1).
-std::pair<int, int> tile_range(const TilePlan& plan, int64_t r0, int64_t r1);
+// [first, last) indices of the tiles whose first row lies in [r0, r1) (the
+// shard ending at `rows` takes every remaining tile).
+std::pair<int, int> tile_range(const TilePlan& plan, int64_t r0, int64_t r1, int64_t rows);
 
 }  // namespace pdlp
