@@ -126,6 +126,9 @@ struct SolverParams {
   bool parity_mode = false;  // PDLP_MODE_PARITY: bitwise-reference iterates
   bool use_cuda_graph = true;
   int engine = PDLP_ENGINE_AUTO;
+  int world_size = 1;  // row sharding: this handle is `rank` of `world_size` (one per GPU)
+  int rank = 0;
+  int plan_world = 0;
 
   void validate() const {  // solver.hpp:79-93
     if (!(eps_optimal > 0.0) || !(eps_infeasible > 0.0))
@@ -256,6 +259,9 @@ inline pdlp_params to_c(const SolverParams& p) {
   c.mode = p.parity_mode ? PDLP_MODE_PARITY : PDLP_MODE_FAST;
   c.use_cuda_graph = p.use_cuda_graph ? 1 : 0;
   c.engine = p.engine;
+  c.world_size = p.world_size;
+  c.rank = p.rank;
+  c.plan_world = p.plan_world;
   return c;
 }
 
@@ -342,6 +348,19 @@ class Solver {
     std::vector<double> out(static_cast<std::size_t>(t ? n_ : m_));
     detail::check(pdlp_spmv(h_, op, in.data(), out.data()));
     return out;
+  }
+
+  /// Row sharding, one process per GPU: export this rank's blob, all-gather
+  /// the blobs (MPI, torch.distributed, files), import them in rank order.
+  std::vector<unsigned char> shard_export() const {
+    std::vector<unsigned char> b(static_cast<std::size_t>(pdlp_shard_blob_size()));
+    detail::check(pdlp_shard_export(h_, b.data(), static_cast<int64_t>(b.size())));
+    return b;
+  }
+  void shard_import(const std::vector<std::vector<unsigned char>>& blobs) {
+    std::vector<unsigned char> all;
+    for (const auto& b : blobs) all.insert(all.end(), b.begin(), b.end());
+    detail::check(pdlp_shard_import(h_, all.data(), static_cast<int32_t>(blobs.size())));
   }
 
   pdlp_handle* handle() const { return h_; }

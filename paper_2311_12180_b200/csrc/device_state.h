@@ -143,8 +143,9 @@ struct DevIter {
   double* seq_dy2;   // parity-mode per-row terms (m)
   double* seq_inter; // (m)
   double* seq_dx2;   // (n)
-  const double* red_tab;  // reduction factors 1-(k+1)^-0.3 for the window
-  const double* gro_tab;  // growth factors 1+(k+1)^-0.6
+  // step factors of the window, interleaved: red_tab[2i] = 1-(k+1)^-0.3,
+  // red_tab[2i+1] = 1+(k+1)^-0.6 for k = table_base + i (uploaded with the state)
+  const double* red_tab;
   void* step_log;         // pdlp_step_log_entry[window capacity]
   DevState* st;
   // ---- sharding (world == 1: single device, everything below unused) ----

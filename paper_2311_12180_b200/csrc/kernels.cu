@@ -216,9 +216,9 @@ __global__ void __launch_bounds__(kThreads, 4) dual_kernel(DevCsr K, DevIter it,
   // the primal kernel's CTAs may start their prologue once every dual CTA is
   // past its tile (triggering earlier would let them take slots from our waves)
   griddep_launch_dependents();
-  store_partial<3, 0>(red, it.d_part, tile);
+  store_partial<3, 0>(red, it.d_part, tile, it.d_tiles);
   if (kShard) {
-    push_partial<3>(it.shv->d_part, it.world, it.rank, 0, size_t(tile), red);
+    push_partial<3>(it.shv->d_part, it.world, it.rank, 0, size_t(tile), size_t(it.d_tiles), red);
     shard_signal(it.shv, it.sync, it.world, it.rank, kSyncDual);
     return;
   }
@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 4) dual_kernel(DevCsr K, DevIter it,
   const DevState pre = *st;
   const int64_t ti = pre.total - pre.table_base;
   const Decision d = step_decision(pre, it, dy2, inter, dx2, dpart[2] == 0.0 && ppart[1] == 0.0,
-                                   it.red_tab[ti], it.gro_tab[ti], st);
+                                   it.red_tab[2 * ti], it.red_tab[2 * ti + 1], st);
   __threadfence();
   if (use_cond) cudaGraphSetConditional(cond, d.cont ? 1u : 0u);
 }
@@ -292,8 +292,8 @@ __global__ void __launch_bounds__(kThreads, 4) primal_kernel(DevCsr KT, DevIter 
     if (tid < kWords) w = __ldcg(reinterpret_cast<const unsigned long long*>(it.snap) + tid);
     double tr = 0.0, tg = 0.0, px = 0.0;
     if (tid < kHeadTab) {
-      tr = __ldcg(it.red_tab + tid);
-      tg = __ldcg(it.gro_tab + tid);
+      tr = __ldcg(it.red_tab + 2 * tid);
+      tg = __ldcg(it.red_tab + 2 * tid + 1);
     }
     if (tid < 2) px = __ldcg(it.px_total + tid);
     double dp[3];
@@ -324,8 +324,8 @@ __global__ void __launch_bounds__(kThreads, 4) primal_kernel(DevCsr KT, DevIter 
       } else {
         const bool commit = bid == 0;
         const int64_t ti = s.total - s.table_base;
-        const double rk = ti < kHeadTab ? s_tab[0][ti] : it.red_tab[ti];
-        const double gk = ti < kHeadTab ? s_tab[1][ti] : it.gro_tab[ti];
+        const double rk = ti < kHeadTab ? s_tab[0][ti] : it.red_tab[2 * ti];
+        const double gk = ti < kHeadTab ? s_tab[1][ti] : it.red_tab[2 * ti + 1];
         sd = step_decision(s, it, dp[0], dp[1], s_px[0], dp[2] == 0.0 && s_px[1] == 0.0, rk, gk,
                            commit ? st : nullptr);
         if (commit) {
@@ -415,9 +415,9 @@ __global__ void __launch_bounds__(kThreads, 4) primal_kernel(DevCsr KT, DevIter 
   // ping-pong by trial parity: the next decision reads these while this launch's
   // late CTAs may still be reading the previous ones
   const size_t half = size_t(d.trials & 1) * it.p_tiles * 2;
-  store_partial<2, 0>(red, it.p_part + half, tile);
+  store_partial<2, 0>(red, it.p_part + half, tile, it.p_tiles);
   if (kShard) {
-    push_partial<2>(it.shv->p_part, it.world, it.rank, half, size_t(tile), red);
+    push_partial<2>(it.shv->p_part, it.world, it.rank, half, size_t(tile), size_t(it.p_tiles), red);
     shard_signal(it.shv, it.sync, it.world, it.rank, kSyncPrimal);
   }
 }
@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(kThreads) decide_kernel(DevIter it, cudaGraphC
   const int64_t ti = pre.total - pre.table_base;
   const double px0 = __ldcg(it.px_total), px1 = __ldcg(it.px_total + 1);
   const Decision d = step_decision(pre, it, dp[0], dp[1], px0, dp[2] == 0.0 && px1 == 0.0,
-                                   it.red_tab[ti], it.gro_tab[ti], st);
+                                   it.red_tab[2 * ti], it.red_tab[2 * ti + 1], st);
   __threadfence();
   if (use_cond) cudaGraphSetConditional(cond, d.cont ? 1u : 0u);
 }
@@ -580,7 +580,7 @@ __global__ void __launch_bounds__(kThreads) eval_prep_kernel(DevIter it, DevEval
       red[3] += da * da;
     }
   }
-  store_partial<4, 0>(red, ev.part0, blockIdx.x);
+  store_partial<4, 0>(red, ev.part0, blockIdx.x, ev.grid0);
 }
 
 // Sharded evaluation: this rank's slices of the averages to every peer (the
@@ -742,7 +742,7 @@ struct Ev2Epi : EpiBase<Ev2Epi<kSeq>> {
 };
 
 template <bool kSeq>
-__global__ void __launch_bounds__(kThreads) eval_rows_kernel(DevCsr K, DevEval ev, int m, int m1) {
+__global__ void __launch_bounds__(kThreads, 3) eval_rows_kernel(DevCsr K, DevEval ev, int m, int m1) {
   extern __shared__ __align__(16) unsigned char smem[];
   Ev1Epi<kSeq> epi;
   epi.X4 = ev.X4, epi.Y4 = ev.Y4, epi.q = ev.q, epi.seq_r = ev.seq_r, epi.m = m, epi.m1 = m1;
@@ -753,9 +753,9 @@ __global__ void __launch_bounds__(kThreads) eval_rows_kernel(DevCsr K, DevEval e
   const int ti = K.tile0 + int(blockIdx.x);
   run_tile<Ev1Epi<kSeq>, kSeq>(K.tiles[ti], K.rp, K.col, K.val_orig, epi, red, K.chunk_part,
                                K.chunk_ctr, smem);
-  store_partial<12, 2>(red, ev.part1, ti);
+  store_partial<12, 2>(red, ev.part1, ti, ev.ev1_tiles);
   if (ev.world > 1) {
-    push_partial<14>(ev.shv->part1, ev.world, ev.rank, 0, size_t(ti), red);
+    push_partial<14>(ev.shv->part1, ev.world, ev.rank, 0, size_t(ti), size_t(ev.ev1_tiles), red);
     shard_signal(ev.shv, ev.sync, ev.world, ev.rank, kSyncEvRows);
   }
 }
@@ -774,9 +774,9 @@ __global__ void __launch_bounds__(kThreads) eval_cols_kernel(DevCsr KT, DevEval 
   const int ti = KT.tile0 + int(blockIdx.x);
   run_tile<Ev2Epi<kSeq>, kSeq>(KT.tiles[ti], KT.rp, KT.col, KT.val_orig, epi, red, KT.chunk_part,
                                KT.chunk_ctr, smem);
-  store_partial<14, 4>(red, ev.part2, ti);
+  store_partial<14, 4>(red, ev.part2, ti, ev.ev2_tiles);
   if (ev.world > 1) {
-    push_partial<18>(ev.shv->part2, ev.world, ev.rank, 0, size_t(ti), red);
+    push_partial<18>(ev.shv->part2, ev.world, ev.rank, 0, size_t(ti), size_t(ev.ev2_tiles), red);
     shard_signal(ev.shv, ev.sync, ev.world, ev.rank, kSyncEvCols);
   }
 }

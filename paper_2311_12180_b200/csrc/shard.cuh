@@ -95,13 +95,13 @@ __device__ __forceinline__ void push_peers(double* const* field, int world, int 
 }
 
 // Thread 0 holds a block-reduced partial of width W (after store_partial):
-// copy it to every peer's partial array at the same global slot.
+// copy it to every peer's (component-major) partial array at the same slot.
 template <int W>
 __device__ __forceinline__ void push_partial(double* const* field, int world, int rank, size_t base,
-                                             size_t slot, const double (&v)[W]) {
+                                             size_t slot, size_t stride, const double (&v)[W]) {
   if (threadIdx.x != 0) return;
 #pragma unroll
-  for (int i = 0; i < W; ++i) push_peers(field, world, rank, base + slot * W + i, v[i]);
+  for (int i = 0; i < W; ++i) push_peers(field, world, rank, base + size_t(i) * stride + slot, v[i]);
 }
 
 }  // namespace pdlp

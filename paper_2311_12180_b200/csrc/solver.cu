@@ -443,20 +443,28 @@ void Solver::allocate_iteration() {
   seq_inter_.alloc(seq ? m_ : 1);
   seq_dx2_.alloc(seq ? n_ : 1);
   tab_cap_ = int(std::min<int64_t>(params_.evaluation_frequency, 4096));
-  red_tab_.alloc(std::max(tab_cap_, 128));  // the primal head stages 128 entries
-  gro_tab_.alloc(std::max(tab_cap_, 128));
-  red_tab_.zero(s);
-  gro_tab_.zero(s);
+  {
+    // [EvalOut | DevState | step-factor pairs]: one D2H (eval + state) and one
+    // H2D (state + factors) per window round trip
+    auto up64 = [](size_t b) { return (b + 63) & ~size_t(63); };
+    xo_state_ = up64(sizeof(EvalOut));
+    xo_tab_ = xo_state_ + up64(sizeof(DevState));
+    const size_t bytes = xo_tab_ + 2 * sizeof(double) * size_t(std::max(tab_cap_, 128));  // head stages 128
+    xfer_dev_.alloc(bytes);
+    xfer_dev_.zero(s);
+    xfer_host_.alloc(bytes);
+    std::memset(xfer_host_.get(), 0, bytes);
+    eval_dev_ = reinterpret_cast<EvalOut*>(xfer_dev_.get());
+    state_dev_ = reinterpret_cast<DevState*>(xfer_dev_.get() + xo_state_);
+    he_ = reinterpret_cast<EvalOut*>(xfer_host_.get());
+    hs_ = reinterpret_cast<DevState*>(xfer_host_.get() + xo_state_);
+    tab_host_ = reinterpret_cast<double*>(xfer_host_.get() + xo_tab_);
+  }
   step_log_dev_.alloc(tab_cap_);
-  state_dev_.alloc(1);
   snap_dev_.alloc(1);
   snap_dev_.zero(s);
-  state_dev_.zero(s);
-  hs_.alloc(1);
-  he_.alloc(1);
-  tab_host_.alloc(2 * size_t(tab_cap_));
   log_host_.alloc(tab_cap_);
-  std::memset(hs_.get(), 0, sizeof(DevState));
+
 
   DevIter& it = it_;
   for (int i = 0; i < 3; ++i) {
@@ -501,8 +509,7 @@ void Solver::allocate_iteration() {
   it.seq_dy2 = seq_dy2_.get();
   it.seq_inter = seq_inter_.get();
   it.seq_dx2 = seq_dx2_.get();
-  it.red_tab = red_tab_.get();
-  it.gro_tab = gro_tab_.get();
+  it.red_tab = reinterpret_cast<const double*>(xfer_dev_.get() + xo_tab_);
   it.step_log = step_log_dev_.get();
   // iteration engine
   engine_ = params_.engine;
@@ -520,7 +527,7 @@ void Solver::allocate_iteration() {
     wb_.wp_part = wp_part_.get();
     wb_.bar = bar_.get();
   }
-  it.st = state_dev_.get();
+  it.st = state_dev_;
 
   X4_.alloc(size_t(n_) * 4);
   Y4_.alloc(size_t(m_) * 4);
@@ -533,7 +540,7 @@ void Solver::allocate_iteration() {
   part2_.alloc(size_t(ev2_tiles) * 18);
   seq_r_.alloc(seq ? size_t(m_) * 4 : 1);
   seq_d_.alloc(seq ? size_t(n_) * 4 : 1);
-  eval_dev_.alloc(1);
+
   DevEval& ev = ev_;
   ev.X4 = X4_.get();
   ev.Y4 = Y4_.get();
@@ -551,7 +558,7 @@ void Solver::allocate_iteration() {
   ev.grid0 = grid0;
   ev.seq_r = seq_r_.get();
   ev.seq_d = seq_d_.get();
-  ev.out = eval_dev_.get();
+  ev.out = eval_dev_;
   ev.ev1_tiles = ev1_tiles;
   ev.ev2_tiles = ev2_tiles;
 
@@ -618,12 +625,12 @@ void Solver::capture_window_graph() {
 }
 
 void Solver::upload_state() {
-  PDLP_CUDA(cudaMemcpyAsync(state_dev_.get(), hs_.get(), sizeof(DevState), cudaMemcpyHostToDevice,
+  PDLP_CUDA(cudaMemcpyAsync(state_dev_, hs_, sizeof(DevState), cudaMemcpyHostToDevice,
                             stream_));
 }
 
 void Solver::download_state() {
-  PDLP_CUDA(cudaMemcpyAsync(hs_.get(), state_dev_.get(), sizeof(DevState), cudaMemcpyDeviceToHost,
+  PDLP_CUDA(cudaMemcpyAsync(hs_, state_dev_, sizeof(DevState), cudaMemcpyDeviceToHost,
                             stream_));
   PDLP_CUDA(cudaStreamSynchronize(stream_));
 }
@@ -640,7 +647,7 @@ void Solver::iterate_begin(int32_t* status) {
   PDLP_CUDA(cudaSetDevice(params_.device));
   require_linked();
   t0_ = std::chrono::steady_clock::now();
-  DevState& st = *hs_.get();
+  DevState& st = *hs_;
   std::memset(&st, 0, sizeof st);
   st.eta = eta_hat0_;
   st.eta_acc = eta_hat0_;
@@ -693,7 +700,7 @@ void Solver::iterate_begin(int32_t* status) {
 void Solver::iterate_run(int64_t count, int32_t* status) {
   if (!begun_ || !state_valid_) throw std::logic_error("iterate_run before iterate_begin");
   PDLP_CUDA(cudaSetDevice(params_.device));
-  DevState& st = *hs_.get();
+  DevState& st = *hs_;
   const int64_t freq = params_.evaluation_frequency;
   int64_t done = 0;
   while (!finished_ && done < count) {
@@ -730,25 +737,22 @@ void Solver::iterate_run(int64_t count, int32_t* status) {
 }
 
 void Solver::run_window(int target) {
-  DevState& st = *hs_.get();
-  double* red = tab_host_.get();
-  double* gro = red + tab_cap_;
+  DevState& st = *hs_;
+  double* tab = tab_host_;
   for (int i = 0; i < target; ++i) {
     // factors of adaptive_step_cached for step counter k = total + 1 (solver.hpp:388-390)
     const double kp1 = double(st.total + 1 + i) + 1.0;
-    red[i] = 1.0 - std::pow(kp1, -params_.step_reduction_exponent);
-    gro[i] = 1.0 + std::pow(kp1, -params_.step_growth_exponent);
+    tab[2 * i] = 1.0 - std::pow(kp1, -params_.step_reduction_exponent);
+    tab[2 * i + 1] = 1.0 + std::pow(kp1, -params_.step_growth_exponent);
   }
   st.window_target = target;
   st.window_accepts = 0;
   st.table_base = st.total;
   st.failure = 0;
   const int64_t trials_before = st.trials_total;
-  PDLP_CUDA(cudaMemcpyAsync(red_tab_.get(), red, target * sizeof(double), cudaMemcpyHostToDevice,
-                            stream_));
-  PDLP_CUDA(cudaMemcpyAsync(gro_tab_.get(), gro, target * sizeof(double), cudaMemcpyHostToDevice,
-                            stream_));
-  upload_state();
+  // state + the window's factor pairs in one H2D copy
+  PDLP_CUDA(cudaMemcpyAsync(state_dev_, hs_, xo_tab_ - xo_state_ + 2 * sizeof(double) * size_t(target),
+                            cudaMemcpyHostToDevice, stream_));
   eval_fresh_ = false;
   PDLP_CUDA(cudaEventRecord(ev_w0_, stream_));
   if (engine_ == PDLP_ENGINE_PERSISTENT) {
@@ -784,9 +788,8 @@ void Solver::run_window(int target) {
   PDLP_CUDA(cudaEventRecord(ev_e1_, stream_));
   launches_ += parity() ? 5 : 4;
   ++evaluations_;
-  PDLP_CUDA(cudaMemcpyAsync(hs_.get(), state_dev_.get(), sizeof(DevState), cudaMemcpyDeviceToHost,
-                            stream_));
-  PDLP_CUDA(cudaMemcpyAsync(he_.get(), eval_dev_.get(), sizeof(EvalOut), cudaMemcpyDeviceToHost,
+  // evaluation results + state in one D2H copy
+  PDLP_CUDA(cudaMemcpyAsync(he_, eval_dev_, xo_state_ + sizeof(DevState), cudaMemcpyDeviceToHost,
                             stream_));
   if (st.record_log)
     PDLP_CUDA(cudaMemcpyAsync(log_host_.get(), step_log_dev_.get(),
@@ -813,14 +816,14 @@ void Solver::evaluate() {
   launch_eval(k_ev_.csr, kt_ev_.csr, it_, ev_, parity(), stream_, phase_);
   launches_ += parity() ? 5 : 4;
   ++evaluations_;
-  PDLP_CUDA(cudaMemcpyAsync(he_.get(), eval_dev_.get(), sizeof(EvalOut), cudaMemcpyDeviceToHost,
+  PDLP_CUDA(cudaMemcpyAsync(he_, eval_dev_, sizeof(EvalOut), cudaMemcpyDeviceToHost,
                             stream_));
   PDLP_CUDA(cudaStreamSynchronize(stream_));
   eval_fresh_ = true;
 }
 
 KktHost Solver::kkt(int slot) const {
-  const EvalOut& e = *he_.get();
+  const EvalOut& e = *he_;
   return KktHost{e.prn[slot], e.drn[slot], e.pobj[slot], e.dobj[slot]};
 }
 
@@ -838,8 +841,8 @@ bool Solver::terminated(const KktHost& r) const {
 
 // The evaluation block of SolveLoop::run (solver.hpp:843-927).
 void Solver::evaluation_block() {
-  DevState& st = *hs_.get();
-  const EvalOut& e = *he_.get();
+  DevState& st = *hs_;
+  const EvalOut& e = *he_;
   const KktHost cur = kkt(0), avg = kkt(1);
   const double kc = cur.weighted(st.omega), ka = avg.weighted(st.omega);
   const int cand = !(kc < ka) ? 1 : 0;  // ties go to the average (:718)
@@ -920,7 +923,7 @@ void Solver::evaluation_block() {
 }
 
 void Solver::finish_candidate(int status, const std::string& msg) {
-  const DevState& st = *hs_.get();
+  const DevState& st = *hs_;
   const KktHost cur = kkt(0), avg = kkt(1);
   const int cand = !(cur.weighted(st.omega) < avg.weighted(st.omega)) ? 1 : 0;
   finish(status, cand, cand, cand, cand ? avg : cur, msg);
@@ -931,7 +934,7 @@ void Solver::finish_candidate(int status, const std::string& msg) {
 // of that slot, or -2 for reduced_costs(lp, 0) of a dual-infeasibility exit.
 void Solver::finish(int status, int slot_x, int slot_y, int slot_lam, const KktHost& r,
                     const std::string& msg) {
-  const DevState& st = *hs_.get();
+  const DevState& st = *hs_;
   cudaStream_t s = stream_;
   rx_.assign(n_, 0.0);
   ry_.assign(m_, 0.0);
@@ -1007,7 +1010,7 @@ void Solver::solve(pdlp_result_info* info) {
 void Solver::get_iterate(double* x, double* y, double* kx, double* kty, int64_t* counters,
                          double* scalars) {
   if (!state_valid_) throw std::logic_error("no live iterate (call iterate_begin)");
-  const DevState& st = *hs_.get();
+  const DevState& st = *hs_;
   cudaStream_t s = stream_;
   if (x && n_) PDLP_CUDA(cudaMemcpyAsync(x, it_.x[st.ix_cur], n_ * 8, cudaMemcpyDeviceToHost, s));
   if (y && m_) PDLP_CUDA(cudaMemcpyAsync(y, it_.y[st.iy_cur], m_ * 8, cudaMemcpyDeviceToHost, s));
@@ -1083,7 +1086,7 @@ void Solver::time_kernel(int which, int reps, double* avg_ms, double* bytes) {
   }
   if (which == 2 || which == 3) {
     // plain SpMV microbenchmark on device-resident vectors: 2 = K x, 3 = K^T y
-    const DevState& st = *hs_.get();
+    const DevState& st = *hs_;
     cudaEvent_t e0, e1;
     PDLP_CUDA(cudaEventCreate(&e0));
     PDLP_CUDA(cudaEventCreate(&e1));
@@ -1110,22 +1113,20 @@ void Solver::time_kernel(int which, int reps, double* avg_ms, double* bytes) {
     return;
   }
   reps = std::max(1, std::min(reps, tab_cap_));
-  DevState& st = *hs_.get();
+  DevState& st = *hs_;
   st.failure = 0;
   st.window_accepts = 0;
   st.window_target = 1 << 30;
   st.table_base = st.total;
   st.record_log = 0;
-  double* red = tab_host_.get();
-  double* gro = red + tab_cap_;
+  double* tab = tab_host_;
   for (int i = 0; i < reps; ++i) {
     const double kp1 = double(st.total + 1 + i) + 1.0;
-    red[i] = 1.0 - std::pow(kp1, -params_.step_reduction_exponent);
-    gro[i] = 1.0 + std::pow(kp1, -params_.step_growth_exponent);
+    tab[2 * i] = 1.0 - std::pow(kp1, -params_.step_reduction_exponent);
+    tab[2 * i + 1] = 1.0 + std::pow(kp1, -params_.step_growth_exponent);
   }
-  PDLP_CUDA(cudaMemcpyAsync(red_tab_.get(), red, reps * 8, cudaMemcpyHostToDevice, stream_));
-  PDLP_CUDA(cudaMemcpyAsync(gro_tab_.get(), gro, reps * 8, cudaMemcpyHostToDevice, stream_));
-  upload_state();
+  PDLP_CUDA(cudaMemcpyAsync(state_dev_, hs_, xo_tab_ - xo_state_ + 2 * sizeof(double) * size_t(reps),
+                            cudaMemcpyHostToDevice, stream_));
   // a trial needs a fresh x'; recompute it from the current point
   launch_primal(KT_, it_, parity(), kPRetry, stream_);
   std::vector<cudaEvent_t> ev(2 * reps);

@@ -196,18 +196,22 @@ class Solver {
   DevBuf<double> x_all_, y_all_;  // the three x (3 n) and y (3 m) rotation buffers
   DevBuf<double> kx_[2], kty_[2], avg_x_, avg_y_, x_start_, y_start_;
   DevBuf<double> d_part_, p_part_, seq_dy2_, seq_inter_, seq_dx2_;
-  DevBuf<double> red_tab_, gro_tab_;
+  // one transfer block per window round trip: [EvalOut | DevState | factor pairs]
+  DevBuf<unsigned char> xfer_dev_;
+  PinnedBuf<unsigned char> xfer_host_;
+  size_t xo_state_ = 0, xo_tab_ = 0;
   DevBuf<pdlp_step_log_entry> step_log_dev_;
-  DevBuf<DevState> state_dev_, snap_dev_;
+  DevState* state_dev_ = nullptr;  // inside xfer_dev_
+  DevBuf<DevState> snap_dev_;
   DevBuf<double> X4_, Y4_, lam_, part0_, part1_, part2_, seq_r_, seq_d_, scratch_n_, scratch_m_;
-  DevBuf<EvalOut> eval_dev_;
+  EvalOut* eval_dev_ = nullptr;  // inside xfer_dev_
   DevIter it_{};
   DevEval ev_{};
   int tab_cap_ = 0;
 
-  PinnedBuf<DevState> hs_;
-  PinnedBuf<EvalOut> he_;
-  PinnedBuf<double> tab_host_;
+  DevState* hs_ = nullptr;   // pinned, inside xfer_host_
+  EvalOut* he_ = nullptr;
+  double* tab_host_ = nullptr;
   PinnedBuf<pdlp_step_log_entry> log_host_;
 
   cudaGraph_t graph_ = nullptr;

@@ -312,14 +312,16 @@ __device__ void run_tile(const Tile& t, const int* __restrict__ rp, const int* _
 }
 
 // Block-reduces `red` in fixed order (NS sums then NM maxima) and writes it as
-// partial `slot` (NS+NM doubles).
+// partial `slot`. Partial arrays are component-major ([NS+NM][stride], stride =
+// the array's partial count), so sum_partials reads them coalesced.
 template <int NS, int NM>
-__device__ __forceinline__ void store_partial(double (&red)[NS + NM], double* partials, int slot) {
+__device__ __forceinline__ void store_partial(double (&red)[NS + NM], double* partials, int slot,
+                                              int stride) {
   __shared__ double sred[kWarps * (NS + NM)];
   block_reduce<NS, NM>(red, sred);
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int i = 0; i < NS + NM; ++i) partials[size_t(slot) * (NS + NM) + i] = red[i];
+    for (int i = 0; i < NS + NM; ++i) partials[size_t(i) * stride + slot] = red[i];
   }
 }
 
@@ -340,8 +342,8 @@ __device__ __forceinline__ bool grid_last_block(unsigned* counter, unsigned tota
   return is_last;
 }
 
-// Fixed-order reduction of `count` partials of width NS+NM (single CTA); the
-// result is valid in thread 0.
+// Fixed-order reduction of `count` component-major partials of width NS+NM
+// (single CTA); the result is valid in thread 0.
 template <int NS, int NM>
 __device__ __forceinline__ void sum_partials(const double* partials, int count, double (&out)[NS + NM]) {
   constexpr int K = NS + NM;
@@ -356,7 +358,7 @@ __device__ __forceinline__ void sum_partials(const double* partials, int count, 
       const int j = j0 + b * kThreads;
 #pragma unroll
       for (int i = 0; i < K; ++i)
-        v[b][i] = j < count ? __ldcg(partials + size_t(j) * K + i) : (i < NS ? 0.0 : -INFINITY);
+        v[b][i] = j < count ? __ldcg(partials + size_t(i) * count + j) : (i < NS ? 0.0 : -INFINITY);
     }
 #pragma unroll
     for (int b = 0; b < B; ++b) {

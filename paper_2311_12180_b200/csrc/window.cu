@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(kThreads, 2) window_kernel(DevCsr K, DevCsr KT
       staged_tile(t, sg, sm.prod, de, dred, K.chunk_part, K.chunk_ctr);
       consume_end();
     }
-    store_partial<3, 0>(dred, wb.wd_part, cta);
+    store_partial<3, 0>(dred, wb.wd_part, cta, nctas);
 
     // ---- barrier + step decision by the last CTA (solver.hpp:436-466) ----
     grid_barrier(wb.bar, unsigned(nctas), [&]() {
@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, 2) window_kernel(DevCsr K, DevCsr KT
         const double ia = fabs(inter);
         const double eta_bar = ia > 0.0 ? movement / (2.0 * ia) : INFINITY;
         const int64_t ti = st->total - st->table_base;
-        const double eta_next = smin(it.red_tab[ti] * eta_bar, it.gro_tab[ti] * eta);
+        const double eta_next = smin(it.red_tab[2 * ti] * eta_bar, it.red_tab[2 * ti + 1] * eta);
         if (eta <= eta_bar) {
           if (st->record_log) {
             pdlp_step_log_entry* log = reinterpret_cast<pdlp_step_log_entry*>(it.step_log);
@@ -511,7 +511,7 @@ __global__ void __launch_bounds__(kThreads, 2) window_kernel(DevCsr K, DevCsr KT
         pred[1] += isfinite(xn) ? 0.0 : 1.0;
       }
     }
-    store_partial<2, 0>(pred, wb.wp_part, cta);
+    store_partial<2, 0>(pred, wb.wp_part, cta, nctas);
     p_src = wb.wp_part;
     p_count = nctas;
     if (!cont) break;
