@@ -62,6 +62,16 @@ __device__ __forceinline__ int4 ld_stream_i4(const int* p) {
                : "l"(p));
   return r;
 }
+__device__ __forceinline__ int ld_stream_i1(const int* p) {
+  int r;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ double ld_stream_d1(const double* p) {
+  double r;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  return r;
+}
 __device__ __forceinline__ double2 ld_stream_d2(const double* p) {
   double2 r;
   asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"

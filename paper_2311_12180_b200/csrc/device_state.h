@@ -138,6 +138,7 @@ struct DevIter {
   double* px_total;  // unused (kept for layout stability)
   DevState* snap;    // state the current trial's dual kernel ran on (fast mode)
   int d_tiles;       // global K tiles (dual partials the decision sums)
+  int kty_lazy;      // 1: accepted steps do not store K'y' (recomputed by a retry)
   int decide_sep;    // 1: the step decision runs in its own one-CTA kernel (many
                      //    tiles); 0: every primal CTA recomputes it at its head
   double* seq_dy2;   // parity-mode per-row terms (m)

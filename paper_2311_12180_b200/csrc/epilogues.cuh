@@ -148,12 +148,13 @@ struct PrimalEpi : EpiBase<PrimalEpi<kSeq, kNonneg, kCoh, kShard>> {
   double ratio;
   int do_avg;
   int avg_first;
+  int store_kty;  // 0: K'y' of an accepted step is not kept (kty_lazy)
   PeerPush push;  // x' to every peer (kShard)
   __device__ __forceinline__ void gather(int r, double (&g)[1]) const { g[0] = ldv<kCoh>(yg + r); }
   __device__ __forceinline__ void add(double (&a)[1], const double (&p)[1], int) const { a[0] += p[0]; }
   __device__ __forceinline__ void row_done(int j, const double (&a)[1], double (&red)[2]) const {
     const double s = a[0];
-    kty_out[j] = s;
+    if (store_kty) kty_out[j] = s;
     const double xa = ldv<kCoh>(xc + j);
     if (do_avg) avg_x[j] = avg_first ? xa : avg_x[j] + ratio * (xa - avg_x[j]);
     const double v = xa - tau * (c[j] - s);  // solver.hpp:404-408
@@ -203,7 +204,7 @@ struct PrimalEpi : EpiBase<PrimalEpi<kSeq, kNonneg, kCoh, kShard>> {
       red[0] += dd;
       red[1] += isfinite(xn4[i]) ? 0.0 : 1.0;
     }
-    st2(kty_out + j0, s4);
+    if (store_kty) st2(kty_out + j0, s4);
     st2(xt + j0, xn4);
     if (kShard)
       for (int i = 0; i < 4; ++i) push(j0 + i, xn4[i]);
@@ -232,7 +233,7 @@ struct PrimalEpi : EpiBase<PrimalEpi<kSeq, kNonneg, kCoh, kShard>> {
       if (i < nvalid) {
         const int j = j0 + i * stride;
         const double s = acc[i][0];
-        kty_out[j] = s;
+        if (store_kty) kty_out[j] = s;
         if (do_avg) avg_x[j] = avg_first ? xa[i] : av[i] + ratio * (xa[i] - av[i]);
         const double v = xa[i] - tau * (cc[i] - s);  // solver.hpp:404-408
         const double xn = kNonneg ? smax(v, 0.0) : clamp_box(v, ll[i], uu[i]);

@@ -357,7 +357,10 @@ __global__ void __launch_bounds__(kThreads, 4) primal_kernel(DevCsr KT, DevIter 
     return;
   }
   const Tile t = KT.tiles[tile];
-  if (d.mode == kPAccept || d.mode == kPRestart) {
+  // kty_lazy: an accepted step keeps no K'y'; a later rejected trial recomputes
+  // it (the SpMV branch below, without the averages) before its x'
+  const bool lazy_retry = !kSeq && it.kty_lazy && d.mode == kPRetry && mode_override < 0;
+  if (d.mode == kPAccept || d.mode == kPRestart || lazy_retry) {
     const bool acc = d.mode == kPAccept;
     {
       // the epilogue's contiguous operands of this tile's columns -> L2 while
@@ -388,6 +391,7 @@ __global__ void __launch_bounds__(kThreads, 4) primal_kernel(DevCsr KT, DevIter 
     epi.ratio = d.ratio;
     epi.do_avg = acc;
     epi.avg_first = d.first;
+    epi.store_kty = (acc && !kSeq && it.kty_lazy) ? 0 : 1;
     epi.push = push;
     run_tile<PrimalEpi<kSeq, kNonneg, false, kShard>, kSeq>(t, KT.rp, KT.col, KT.val, epi, red,
                                                             KT.chunk_part, KT.chunk_ctr, smem);
@@ -986,6 +990,22 @@ __global__ void gather_transpose_kernel(const int* perm, const int* row_of, cons
   }
 }
 
+// Planner input: does row r have mostly consecutive columns (and more than
+// min_len entries)? One warp per row.
+__global__ void row_contig_kernel(const int* rp, const int* col, int rows, int min_len,
+                                  unsigned char* out) {
+  const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= rows) return;
+  const int k0 = rp[w], k1 = rp[w + 1];
+  int cnt = 0;
+  if (k1 - k0 > min_len)
+    for (int k = k0 + lane; k + 1 < k1; k += 32) cnt += (col[k + 1] == col[k] + 1) ? 1 : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if (lane == 0) out[w] = (k1 - k0 > min_len && 2 * cnt >= k1 - k0 - 1) ? 1 : 0;
+}
+
 __global__ void fill_kernel(double* p, int64_t n, double v) {
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += stride) p[k] = v;
@@ -1149,6 +1169,13 @@ void launch_count_cols(const int* col, int64_t nnz, int* counts, cudaStream_t s)
 void launch_gather_transpose(const int* perm, const int* row_of, const double* val, int64_t nnz,
                              int* col_t, double* val_t, cudaStream_t s) {
   gather_transpose_kernel<<<grid_for(nnz), kThreads, 0, s>>>(perm, row_of, val, nnz, col_t, val_t);
+  PDLP_CUDA(cudaGetLastError());
+}
+void launch_row_contig(const int* rp, const int* col, int rows, int min_len, unsigned char* out,
+                       cudaStream_t s) {
+  const int64_t threads = int64_t(rows) * 32;
+  const int64_t grid = (threads + kThreads - 1) / kThreads;
+  if (grid > 0) row_contig_kernel<<<unsigned(grid), kThreads, 0, s>>>(rp, col, rows, min_len, out);
   PDLP_CUDA(cudaGetLastError());
 }
 void launch_fill(double* p, int64_t n, double v, cudaStream_t s) {

@@ -252,12 +252,30 @@ void Solver::setup(const pdlp_lp& lp) {
   const int64_t c0 = world_ > 1 ? kt_cuts_[rank_] : 0, c1 = world_ > 1 ? kt_cuts_[rank_ + 1] : n_;
   // three tilings of each operator: iteration kernels, persistent window
   // kernel, evaluation kernels (common.cuh TileGeom)
-  build_plan(k_it_, K_, rp_h, kIterGeom, kbrk, r0, r1);
-  build_plan(kt_it_, KT_, rpt_h, kIterGeom, ktbrk, c0, c1);
+  // rows with mostly consecutive columns get element-interleaved lane groups
+  std::vector<uint8_t> kcon, ktcon;
+  const std::vector<uint8_t>* kc_p = nullptr;
+  const std::vector<uint8_t>* ktc_p = nullptr;
+  // (measured on C2: -7% SpMV time over K but a different rounding trajectory;
+  // opt-in until the dual kernel's other costs shrink)
+  if (!parity() && std::getenv("PDLP_CONTIG")) {
+    DevBuf<unsigned char> f1{static_cast<size_t>(m_)}, f2{static_cast<size_t>(n_)};
+    launch_row_contig(k_rp_.get(), k_col_.get(), int(m_), kStreamMaxRow, f1.get(), s);
+    launch_row_contig(kt_rp_.get(), kt_col_.get(), int(n_), kStreamMaxRow, f2.get(), s);
+    kcon.resize(size_t(m_));
+    ktcon.resize(size_t(n_));
+    if (m_) PDLP_CUDA(cudaMemcpyAsync(kcon.data(), f1.get(), size_t(m_), cudaMemcpyDeviceToHost, s));
+    if (n_) PDLP_CUDA(cudaMemcpyAsync(ktcon.data(), f2.get(), size_t(n_), cudaMemcpyDeviceToHost, s));
+    PDLP_CUDA(cudaStreamSynchronize(s));
+    kc_p = &kcon;
+    ktc_p = &ktcon;
+  }
+  build_plan(k_it_, K_, rp_h, kIterGeom, kbrk, r0, r1, kc_p);
+  build_plan(kt_it_, KT_, rpt_h, kIterGeom, ktbrk, c0, c1, ktc_p);
   build_plan(k_win_, K_, rp_h, kWinGeom, {}, 0, m_);
   build_plan(kt_win_, KT_, rpt_h, kWinGeom, {}, 0, n_);
-  build_plan(k_ev_, K_, rp_h, kEvalGeom, kbrk, r0, r1);
-  build_plan(kt_ev_, KT_, rpt_h, kEvalGeom, ktbrk, c0, c1);
+  build_plan(k_ev_, K_, rp_h, kEvalGeom, kbrk, r0, r1, kc_p);
+  build_plan(kt_ev_, KT_, rpt_h, kEvalGeom, ktbrk, c0, c1, ktc_p);
   K_ = k_it_.csr;
   KT_ = kt_it_.csr;
   K_full_ = K_;
@@ -285,7 +303,7 @@ void Solver::setup(const pdlp_lp& lp) {
 
 void Solver::build_plan(OpPlan& p, const DevCsr& base, const std::vector<int>& rp,
                         const TileGeom& g, const std::vector<int64_t>& breaks, int64_t r0,
-                        int64_t r1) {
+                        int64_t r1, const std::vector<uint8_t>* contig) {
   // planner thresholds: env overrides are a tuning aid (clamped to the geometry)
   auto knob = [](const char* name, int def) {
     const char* v = std::getenv(name);
@@ -296,7 +314,7 @@ void Solver::build_plan(OpPlan& p, const DevCsr& base, const std::vector<int>& r
   const int cnnz = std::min(knob("PDLP_CHUNK_NNZ", g.chunk_nnz), g.chunk_nnz);
   const int lane = std::min(knob("PDLP_LANE_NNZ", g.lane_nnz), g.lane_nnz);
   p.plan = plan_tiles<int>(int64_t(rp.size()) - 1, rp.data(), parity(), smax, wmax, cnnz,
-                           g.stream_nnz, g.stream_rows, kThreads, lane, breaks);
+                           g.stream_nnz, g.stream_rows, kThreads, lane, breaks, contig);
   const std::vector<Tile>& th = p.plan.tiles;
   p.tiles.alloc(th.size());
   PDLP_CUDA(cudaMemcpyAsync(p.tiles.get(), th.data(), th.size() * sizeof(Tile),
@@ -515,6 +533,9 @@ void Solver::allocate_iteration() {
   engine_ = params_.engine;
   if (engine_ == PDLP_ENGINE_AUTO)
     engine_ = params_.use_cuda_graph ? PDLP_ENGINE_GRAPH : PDLP_ENGINE_STREAM;
+  // fast per-trial kernels skip storing K'y' on accepted steps (8n bytes per
+  // iteration); the persistent window kernel keeps its own cache
+  it.kty_lazy = (!parity() && engine_ != PDLP_ENGINE_PERSISTENT && !std::getenv("PDLP_NO_LAZY_KTY")) ? 1 : 0;
   if (engine_ == PDLP_ENGINE_PERSISTENT && parity())
     invalid("params: the persistent engine runs fast mode only");
   if (engine_ == PDLP_ENGINE_PERSISTENT) {
@@ -1016,8 +1037,12 @@ void Solver::get_iterate(double* x, double* y, double* kx, double* kty, int64_t*
   if (y && m_) PDLP_CUDA(cudaMemcpyAsync(y, it_.y[st.iy_cur], m_ * 8, cudaMemcpyDeviceToHost, s));
   if (kx && m_)
     PDLP_CUDA(cudaMemcpyAsync(kx, kx_[st.ikx_cur].get(), m_ * 8, cudaMemcpyDeviceToHost, s));
-  if (kty && n_)
+  if (kty && n_) {
+    // lazily kept K'y': recompute it for the current y (same tiles and order
+    // as the primal kernel, so bitwise what it would have stored)
+    if (it_.kty_lazy) launch_spmv(KT_full_, false, it_.y[st.iy_cur], it_.kty[st.ikty_cur], parity(), s);
     PDLP_CUDA(cudaMemcpyAsync(kty, kty_[st.ikty_cur].get(), n_ * 8, cudaMemcpyDeviceToHost, s));
+  }
   PDLP_CUDA(cudaStreamSynchronize(s));
   if (counters) {
     counters[0] = st.total;

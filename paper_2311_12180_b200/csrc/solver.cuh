@@ -152,7 +152,8 @@ class Solver {
     DevCsr csr{};
   };
   void build_plan(OpPlan& p, const DevCsr& base, const std::vector<int>& rp, const TileGeom& g,
-                  const std::vector<int64_t>& breaks, int64_t r0, int64_t r1);
+                  const std::vector<int64_t>& breaks, int64_t r0, int64_t r1,
+                  const std::vector<uint8_t>* contig = nullptr);
   void shard_view_upload();
   void phase() {
     if (phase_) phase_();

@@ -131,6 +131,41 @@ __device__ __forceinline__ void strided_partial(const Epi& epi, const int* __res
   }
 }
 
+// Element-interleaved partial sum over [k0, k1): lane t takes elements
+// k0 + t, k0 + t + nthreads, ... so neighbouring lanes gather neighbouring
+// columns (one L1 wavefront per 32 gathers when a row's columns are
+// contiguous, instead of one per quad-strided lane). Used for WARP tiles whose
+// rows the planner found column-contiguous (Tile::slot == 1).
+template <class Epi>
+__device__ __forceinline__ void elem_partial(const Epi& epi, const int* __restrict__ col,
+                                             const double* __restrict__ val, int k0, int k1, int t,
+                                             int nthreads, double (&acc)[Epi::NA]) {
+  constexpr int U = 4;
+  zero_acc<Epi>(acc);
+  for (int e0 = k0 + t; e0 < k1; e0 += nthreads * U) {
+    int cs[U];
+    double vs[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * nthreads;
+      cs[u] = e < k1 ? ld_stream_i1(col + e) : 0;
+      vs[u] = e < k1 ? ld_stream_d1(val + e) : 0.0;
+    }
+    double g[U][Epi::NP];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (e0 + u * nthreads < k1) epi.gather(cs[u], g[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (e0 + u * nthreads < k1) {
+        double p[Epi::NP];
+#pragma unroll
+        for (int j = 0; j < Epi::NP; ++j) p[j] = vs[u] * g[u][j];
+        epi.add(acc, p, cs[u]);
+      }
+  }
+}
+
 // Pulls a tile's static operator data (offsets, indices, values) toward L2
 // before griddep_wait(), so the loads after it overlap the predecessor's tail.
 __device__ __forceinline__ void prefetch_tile(const Tile& t, const int* rp, const int* col,
@@ -240,6 +275,8 @@ __device__ void run_tile(const Tile& t, const int* __restrict__ rp, const int* _
       const int k0 = rp[r], k1 = rp[r + 1];
       if (kSeq) {
         if (lane == 0) row_sum_sequential(epi, col, val, k0, k1, acc);
+      } else if (t.slot == 1) {
+        elem_partial(epi, col, val, k0, k1, lane, G, acc);
       } else {
         strided_partial(epi, col, val, k0, k1, lane, G, acc);
       }

@@ -10,7 +10,11 @@ namespace pdlp {
 template <class Off>
 TilePlan plan_tiles(int64_t rows, const Off* rp, bool parity, int stream_max_row,
                     int warp_max_row, int chunk_nnz, int stream_nnz, int stream_rows, int threads,
-                    int lane_nnz, const std::vector<int64_t>& breaks) {
+                    int lane_nnz, const std::vector<int64_t>& breaks,
+                    const std::vector<uint8_t>* contig) {
+  // rows whose columns are mostly consecutive (contig[r] != 0) get
+  // element-interleaved WARP tiles; others quad-strided ones
+  auto cflag = [&](int64_t i) { return contig && (*contig)[size_t(i)] ? 1 : 0; };
   TilePlan plan;
   int64_t r = 0;
   size_t bi = 0;
@@ -38,10 +42,11 @@ TilePlan plan_tiles(int64_t rows, const Off* rp, bool parity, int stream_max_row
       };
       const int g = lanes(l);
       const int64_t r0 = r;
+      const int cf = cflag(r);
       while (r < brk && r - r0 < threads / g && len(r) > stream_max_row && len(r) <= warp_max_row &&
-             lanes(len(r)) == g)
+             lanes(len(r)) == g && cflag(r) == cf)
         ++r;
-      plan.tiles.push_back({kTileWarp, int32_t(r0), int32_t(r), int32_t(rp[r0]), int32_t(rp[r]), g, 1, 0});
+      plan.tiles.push_back({kTileWarp, int32_t(r0), int32_t(r), int32_t(rp[r0]), int32_t(rp[r]), g, 1, cf});
       ++plan.warp_tiles;
     } else {
       const int64_t k0 = rp[r], k1 = rp[r + 1];
@@ -107,9 +112,9 @@ std::pair<int, int> tile_range(const TilePlan& plan, int64_t r0, int64_t r1, int
 }
 
 template TilePlan plan_tiles<int>(int64_t, const int*, bool, int, int, int, int, int, int, int,
-                                  const std::vector<int64_t>&);
+                                  const std::vector<int64_t>&, const std::vector<uint8_t>*);
 template TilePlan plan_tiles<int64_t>(int64_t, const int64_t*, bool, int, int, int, int, int, int,
-                                      int, const std::vector<int64_t>&);
+                                      int, const std::vector<int64_t>&, const std::vector<uint8_t>*);
 template std::vector<int64_t> shard_cuts<int>(int64_t, const int*, int);
 template std::vector<int64_t> shard_cuts<int64_t>(int64_t, const int64_t*, int);
 

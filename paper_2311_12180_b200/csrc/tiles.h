@@ -32,7 +32,7 @@ struct Tile {
   int32_t k1;
   int32_t part;
   int32_t nparts;
-  int32_t slot;   // CHUNK: first partial slot of the row
+  int32_t slot;   // CHUNK: first partial slot of the row; WARP: 1 = element-interleaved lanes
 };
 static_assert(sizeof(Tile) == 32, "tile descriptor is 32 bytes");
 
@@ -50,7 +50,8 @@ struct TilePlan {
 template <class Off>
 TilePlan plan_tiles(int64_t rows, const Off* rp, bool parity, int stream_max_row,
                     int warp_max_row, int chunk_nnz, int stream_nnz, int stream_rows, int threads,
-                    int lane_nnz, const std::vector<int64_t>& breaks = {});
+                    int lane_nnz, const std::vector<int64_t>& breaks = {},
+                    const std::vector<uint8_t>* contig = nullptr);
 
 // Shard boundaries: world + 1 rows 0 = c_0 < c_1 < ... < c_world = rows,
 // balancing nnz + rows per shard, interior cuts on multiples of 4 rows.

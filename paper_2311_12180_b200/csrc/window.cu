@@ -469,6 +469,7 @@ __global__ void __launch_bounds__(kThreads, 2) window_kernel(DevCsr K, DevCsr KT
       pe.l = it.l;
       pe.u = it.u;
       pe.kty_out = it.kty[st->ikty_cur];
+      pe.store_kty = 1;
       pe.xt = it.x[st->ix_trial];
       pe.avg_x = it.avg_x;
       pe.seq_dx2 = nullptr;
