@@ -150,7 +150,7 @@ typedef struct {
   int32_t device;              /* CUDA ordinal, default 0 */
   int32_t mode;                /* PDLP_MODE_FAST */
   int32_t use_cuda_graph;      /* 1: replay each evaluation window as a CUDA graph */
-  int32_t l2_persist;          /* 1: pin the gathered iterate in L2 (access-policy window) */
+  int32_t l2_persist;          /* 1: pin the gathered iterate in L2 (access-policy window); default 0 */
   int32_t engine;              /* PDLP_ENGINE_*: how a window of iterations is driven */
   /* Row sharding: this handle is rank `rank` of `world_size`
    * ranks (one per GPU), each running its contiguous share of the rows of K

@@ -82,7 +82,7 @@ void pdlp_default_params(pdlp_params* p) {
   p->device = 0;
   p->mode = PDLP_MODE_FAST;
   p->use_cuda_graph = 1;
-  p->l2_persist = 1;
+  p->l2_persist = 0;  /* opt-in: measured neutral on C2, -2% on C3 */
   p->engine = PDLP_ENGINE_AUTO;
   p->world_size = 1;
   p->rank = 0;

@@ -133,6 +133,7 @@ struct DualEpi : EpiBase<DualEpi<kSeq, kCoh, kShard>> {
 template <bool kSeq, bool kNonneg, bool kCoh = false, bool kShard = false>
 struct PrimalEpi : EpiBase<PrimalEpi<kSeq, kNonneg, kCoh, kShard>> {
   static constexpr int NP = 1, NA = 1, NR = 2;
+  static constexpr bool kUniform = !kCoh;  // K^T rows are often uniform (2 per column in C2, 5 in C1/C4)
   static constexpr TileGeom kGeom = kIterGeom;
   static constexpr bool kNeedCol = false;
   const double* __restrict__ yg;

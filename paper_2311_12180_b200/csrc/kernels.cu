@@ -159,6 +159,23 @@ __device__ Decision step_decision(const DevState& s, const DevIter& it, double d
   return d;
 }
 
+// decide_sep == 2: the last dual CTA to finish sums the dual partials once and
+// commits the step decision (same sums and order as every other placement).
+__device__ __forceinline__ void dual_tail_decision(const DevIter& it, DevState* st,
+                                                   cudaGraphConditionalHandle cond, int use_cond) {
+  if (!grid_last_block(&st->ctr_dual, gridDim.x)) return;
+  double dp[3];
+  sum_partials<3, 0>(it.d_part, it.d_tiles, dp);
+  if (threadIdx.x != 0) return;
+  const DevState pre = *st;
+  const int64_t ti = pre.total - pre.table_base;
+  const double px0 = __ldcg(it.px_total), px1 = __ldcg(it.px_total + 1);
+  const Decision d = step_decision(pre, it, dp[0], dp[1], px0, dp[2] == 0.0 && px1 == 0.0,
+                                   it.red_tab[2 * ti], it.red_tab[2 * ti + 1], st);
+  __threadfence();
+  if (use_cond) cudaGraphSetConditional(cond, d.cont ? 1u : 0u);
+}
+
 // Dual side of a trial: K x' fused with the projected dual update and the dy^2 /
 // interaction partials. In fast mode the step decision is taken at the head of
 // the primal kernel (every primal CTA recomputes it from the same partials in
@@ -170,9 +187,12 @@ __global__ void __launch_bounds__(kThreads, 4) dual_kernel(DevCsr K, DevIter it,
                                                            cudaGraphConditionalHandle cond,
                                                            int use_cond) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int tile = K.tile0 + int(blockIdx.x);  // global tile index (partials, sharding)
-  const Tile t = K.tiles[tile];
-  prefetch_tile(t, K.rp, K.col, K.val);
+  // fast mode: CTA 0 is a helper (state snapshot, dx^2 of x') running beside
+  // the tile CTAs 1..ntiles instead of delaying one of them
+  const bool helper = !kSeq && blockIdx.x == 0;
+  const int tile = K.tile0 + int(blockIdx.x) - (kSeq ? 0 : 1);  // global tile index
+  const Tile t = K.tiles[helper ? K.tile0 : tile];
+  if (!helper) prefetch_tile(t, K.rp, K.col, K.val);
   griddep_wait();  // x' and the state come from the previous primal kernel
   DevState* st = it.st;
   // A failed or completed window parks the remaining (stream-engine) launches;
@@ -183,7 +203,7 @@ __global__ void __launch_bounds__(kThreads, 4) dual_kernel(DevCsr K, DevIter it,
     if (blockIdx.x == 0 && threadIdx.x == 0) st->failure = 1;
     parked = true;
   }
-  if (!kSeq && blockIdx.x == 0) {
+  if (helper) {
     if (threadIdx.x == 0) *it.snap = *st;
     // the primal partials of x' (the decision's dx^2) are reduced here, off the
     // critical path, so the decision at the primal head has one round trip
@@ -196,6 +216,14 @@ __global__ void __launch_bounds__(kThreads, 4) dual_kernel(DevCsr K, DevIter it,
   }
   if (parked) {
     if (kSeq && blockIdx.x == 0 && threadIdx.x == 0) st->p_mode = kPNone;
+    return;
+  }
+  if (helper) {
+    if (kShard) {
+      shard_signal(it.shv, it.sync, it.world, it.rank, kSyncDual);
+      return;
+    }
+    if (it.decide_sep == 2) dual_tail_decision(it, st, cond, use_cond);
     return;
   }
   DualEpi<kSeq, false, kShard> epi;
@@ -222,7 +250,10 @@ __global__ void __launch_bounds__(kThreads, 4) dual_kernel(DevCsr K, DevIter it,
     shard_signal(it.shv, it.sync, it.world, it.rank, kSyncDual);
     return;
   }
-  if (!kSeq) return;
+  if (!kSeq) {
+    if (it.decide_sep == 2) dual_tail_decision(it, st, cond, use_cond);
+    return;
+  }
 
   // ---- parity mode: the decision in the last CTA, sums in reference order ----
   if (!grid_last_block(&st->ctr_dual, gridDim.x)) return;
@@ -467,6 +498,7 @@ __global__ void __launch_bounds__(kThreads) decide_kernel(DevIter it, cudaGraphC
 
 struct MatvecEpi : EpiBase<MatvecEpi> {
   static constexpr int NP = 1, NA = 1, NR = 1;
+  static constexpr bool kUniform = true;
   static constexpr TileGeom kGeom = kIterGeom;
   static constexpr bool kNeedCol = false;
   const double* __restrict__ x;
@@ -1264,9 +1296,9 @@ void launch_dual(const DevCsr& k, const DevIter& it, bool seq, unsigned long lon
   if (seq)
     launch_pdl(dual_kernel<true, false>, k.ntiles, sm, s, k, it, h, use_cond);
   else if (it.world > 1)
-    launch_pdl(dual_kernel<false, true>, k.ntiles, sm, s, k, it, h, use_cond);
+    launch_pdl(dual_kernel<false, true>, k.ntiles + 1, sm, s, k, it, h, use_cond);
   else
-    launch_pdl(dual_kernel<false, false>, k.ntiles, sm, s, k, it, h, use_cond);
+    launch_pdl(dual_kernel<false, false>, k.ntiles + 1, sm, s, k, it, h, use_cond);
 }
 
 void launch_decide(const DevIter& it, cudaStream_t s, unsigned long long cond, int use_cond) {

@@ -299,6 +299,7 @@ void Solver::setup(const pdlp_lp& lp) {
 
   allocate_iteration();
   set_kernel_attributes();
+  pin_iterates_in_l2();
 }
 
 void Solver::build_plan(OpPlan& p, const DevCsr& base, const std::vector<int>& rp,
@@ -438,6 +439,35 @@ void Solver::precondition() {
   omega0_ = sclamp(w, params_.omega_min, params_.omega_max);
 }
 
+// The iterate buffers the SpMVs gather from (x for K x', y for K'y') stay in
+// L2 across the matrix streams: an access-policy window on the solver's stream
+// (captured into the graph's kernel nodes) marks them persisting, sized to the
+// device's persisting carve-out (hitRatio < 1 when the buffers are larger).
+void Solver::pin_iterates_in_l2() {
+  l2_window_bytes_ = 0;
+  if (!params_.l2_persist || std::getenv("PDLP_NO_L2_PERSIST")) return;
+  int max_persist = 0, max_window = 0;
+  PDLP_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, params_.device));
+  PDLP_CUDA(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, params_.device));
+  if (max_persist <= 0 || max_window <= 0) return;
+  // the larger gather source: x for the dual kernel's K x' (n >= m in every
+  // config), else y; all three rotation buffers (one allocation)
+  const bool use_x = n_ >= m_;
+  void* base = use_x ? static_cast<void*>(x_all_.get()) : static_cast<void*>(y_all_.get());
+  const size_t bytes = 3 * sizeof(double) * size_t(use_x ? n_ : m_);
+  const size_t window = std::min(bytes, size_t(max_window));
+  const size_t carve = std::min(window, size_t(max_persist));
+  PDLP_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve));
+  cudaStreamAttrValue v = {};
+  v.accessPolicyWindow.base_ptr = base;
+  v.accessPolicyWindow.num_bytes = window;
+  v.accessPolicyWindow.hitRatio = float(double(carve) / double(window));
+  v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  PDLP_CUDA(cudaStreamSetAttribute(stream_, cudaStreamAttributeAccessPolicyWindow, &v));
+  l2_window_bytes_ = int64_t(carve);
+}
+
 void Solver::allocate_iteration() {
   cudaStream_t s = stream_;
   x_all_.alloc(3 * size_t(n_));
@@ -524,6 +554,8 @@ void Solver::allocate_iteration() {
   // trial a one-CTA decision kernel is cheaper (C3/C4-sized operators)
   it.decide_sep = (!parity() && double(k_tiles) * double(p_grid) > 2.0e6) ? 1 : 0;
   if (const char* e = std::getenv("PDLP_DECIDE_SEP")) it.decide_sep = parity() ? 0 : std::atoi(e);
+  // 2 (decision in the dual's last CTA) needs every partial on this device
+  if (world_ > 1 && it.decide_sep == 2) it.decide_sep = 1;
   it.seq_dy2 = seq_dy2_.get();
   it.seq_inter = seq_inter_.get();
   it.seq_dx2 = seq_dx2_.get();
@@ -637,9 +669,11 @@ void Solver::capture_window_graph() {
   PDLP_CUDA(cudaStreamBeginCaptureToGraph(stream_, body, nullptr, nullptr, 0,
                                           cudaStreamCaptureModeThreadLocal));
   const unsigned long long ch = static_cast<unsigned long long>(h);
-  launch_dual(K_, it_, parity(), ch, it_.decide_sep ? 0 : 1, stream_);
-  if (it_.decide_sep) launch_decide(it_, stream_, ch, 1);
-  launch_primal(KT_, it_, parity(), -1, stream_, ch, it_.decide_sep ? 0 : 1);
+  // whichever kernel takes the step decision sets the WHILE condition
+  const int ds = it_.decide_sep;
+  launch_dual(K_, it_, parity(), ch, (parity() || ds == 2) ? 1 : 0, stream_);
+  if (ds == 1) launch_decide(it_, stream_, ch, 1);
+  launch_primal(KT_, it_, parity(), -1, stream_, ch, (!parity() && ds == 0) ? 1 : 0);
   PDLP_CUDA(cudaStreamEndCapture(stream_, &body));
   PDLP_CUDA(cudaGraphInstantiate(&graph_exec_, graph_, 0));
   cond_handle_ = static_cast<unsigned long long>(h);
@@ -793,7 +827,7 @@ void Solver::run_window(int target) {
       for (int i = 0; i < remaining; ++i) {
         launch_dual(K_, it_, parity(), 0, 0, stream_);
         phase();
-        if (it_.decide_sep) launch_decide(it_, stream_);
+        if (it_.decide_sep == 1) launch_decide(it_, stream_);
         launch_primal(KT_, it_, parity(), -1, stream_);
         phase();
       }
@@ -826,7 +860,7 @@ void Solver::run_window(int target) {
     eval_seconds_ += 1e-3 * double(ms);
   }
   if (engine_ != PDLP_ENGINE_PERSISTENT)
-    launches_ += (it_.decide_sep ? 3 : 2) * (st.trials_total - trials_before);
+    launches_ += (it_.decide_sep == 1 ? 3 : 2) * (st.trials_total - trials_before);
   if (st.record_log && st.window_accepts > 0)
     step_log_.insert(step_log_.end(), log_host_.get(), log_host_.get() + st.window_accepts);
 }
@@ -1159,7 +1193,7 @@ void Solver::time_kernel(int which, int reps, double* avg_ms, double* bytes) {
   for (int r = 0; r < reps; ++r) {
     if (which == 0) PDLP_CUDA(cudaEventRecord(ev[2 * r], stream_));
     launch_dual(K_, it_, parity(), 0, 0, stream_);
-    if (it_.decide_sep) launch_decide(it_, stream_);
+    if (it_.decide_sep == 1) launch_decide(it_, stream_);
     if (which == 0) PDLP_CUDA(cudaEventRecord(ev[2 * r + 1], stream_));
     if (which == 1) PDLP_CUDA(cudaEventRecord(ev[2 * r], stream_));
     launch_primal(KT_, it_, parity(), -1, stream_);

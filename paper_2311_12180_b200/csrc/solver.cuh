@@ -160,6 +160,7 @@ class Solver {
   }
   void require_linked() const;
   void allocate_iteration();
+  void pin_iterates_in_l2();
   void capture_window_graph();
   void upload_state();
   void download_state();
@@ -243,6 +244,7 @@ class Solver {
   std::vector<double> rx_, ry_, rlam_;
 
   // ---- sharding (world_ == 1: a single device) ----
+  int64_t l2_window_bytes_ = 0;  // persisting L2 carve-out for the gathered iterate
   int world_ = 1, rank_ = 0;
   std::vector<int64_t> k_cuts_, kt_cuts_;  // world + 1 row boundaries of K and K^T
   uint64_t plan_hash_ = 0;

@@ -174,10 +174,75 @@ __device__ __forceinline__ void prefetch_tile(const Tile& t, const int* rp, cons
   // 128-byte lines: 32 indices or 16 values per line
   for (int k = k0 + 32 * int(threadIdx.x); k < k1; k += 32 * kThreads) prefetch_l2(col + k);
   for (int k = (t.k0 & ~15) + 16 * int(threadIdx.x); k < k1; k += 16 * kThreads) prefetch_l2(val + k);
-  if (t.kind != kTileChunk) {
+  if (t.kind == kTileWarp || (t.kind == kTileStream && t.part == 0)) {
     const int r = (t.row0 & ~31) + 32 * int(threadIdx.x);
     if (r <= t.row1) prefetch_l2(rp + r);
   }
+}
+
+// Epilogues opt in to the uniform-row path with `static constexpr bool kUniform`
+// (it costs registers; the dual kernel's K rows are rarely uniform).
+template <class Epi, class = void>
+struct has_uniform { static constexpr bool value = false; };
+template <class Epi>
+struct has_uniform<Epi, decltype(void(Epi::kUniform))> { static constexpr bool value = Epi::kUniform; };
+template <class Epi>
+__host__ __device__ constexpr bool uniform_ok() { return has_uniform<Epi>::value; }
+
+// STREAM tile whose rows all have the same short length L (Tile::part): each
+// thread sums its round-robin rows straight from global memory in index order
+// (bitwise the staged path's result) without the shared-memory staging pass.
+// Rows are processed in pairs so a thread keeps 2L loads and gathers in flight.
+template <class Epi, int L>
+__device__ __forceinline__ void uniform_rows(const Tile& t, const int* __restrict__ col,
+                                             const double* __restrict__ val, const Epi& epi,
+                                             double (&red)[Epi::NR]) {
+  constexpr int RPT = Epi::kGeom.stream_rows / kThreads;
+  constexpr int PAIR = L <= 4 ? 2 : 1;
+  const int tid = threadIdx.x;
+  double acc[RPT][Epi::NA];
+  int nvalid = 0;
+#pragma unroll
+  for (int i0 = 0; i0 < RPT; i0 += PAIR) {
+    int cs[PAIR][L];
+    double vs[PAIR][L];
+    double g[PAIR][L][Epi::NP];
+#pragma unroll
+    for (int h = 0; h < PAIR; ++h) {
+      const int r = t.row0 + tid + (i0 + h) * kThreads;
+      const int k = t.k0 + (r - t.row0) * L;
+#pragma unroll
+      for (int j = 0; j < L; ++j) {
+        cs[h][j] = r < t.row1 ? ld_stream_i1(col + k + j) : 0;
+        vs[h][j] = r < t.row1 ? ld_stream_d1(val + k + j) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < PAIR; ++h) {
+      const int r = t.row0 + tid + (i0 + h) * kThreads;
+#pragma unroll
+      for (int j = 0; j < L; ++j)
+        if (r < t.row1) epi.gather(cs[h][j], g[h][j]);
+    }
+#pragma unroll
+    for (int h = 0; h < PAIR; ++h) {
+      const int i = i0 + h;
+      const int r = t.row0 + tid + i * kThreads;
+#pragma unroll
+      for (int a = 0; a < Epi::NA; ++a) acc[i][a] = 0.0;
+      if (r < t.row1) {
+        nvalid = i + 1;
+#pragma unroll
+        for (int j = 0; j < L; ++j) {
+          double p[Epi::NP];
+#pragma unroll
+          for (int q = 0; q < Epi::NP; ++q) p[q] = vs[h][j] * g[h][j][q];
+          epi.add(acc[i], p, cs[h][j]);
+        }
+      }
+    }
+  }
+  epi.template rows_strided<RPT>(t.row0 + tid, kThreads, nvalid, acc, red);
 }
 
 // Processes one tile; `red` holds this thread's reduction terms.
@@ -187,6 +252,15 @@ __device__ void run_tile(const Tile& t, const int* __restrict__ rp, const int* _
                          const double* __restrict__ val, const Epi& epi, double (&red)[Epi::NR],
                          double* chunk_part, unsigned* chunk_ctr, unsigned char* smem) {
   const int tid = threadIdx.x;
+  if (t.kind == kTileStream && t.part >= 1 && t.part <= 5 && Epi::NP == 1 && uniform_ok<Epi>()) {
+    switch (t.part) {
+      case 1: uniform_rows<Epi, 1>(t, col, val, epi, red); return;
+      case 2: uniform_rows<Epi, 2>(t, col, val, epi, red); return;
+      case 3: uniform_rows<Epi, 3>(t, col, val, epi, red); return;
+      case 4: uniform_rows<Epi, 4>(t, col, val, epi, red); return;
+      default: uniform_rows<Epi, 5>(t, col, val, epi, red); return;
+    }
+  }
   if (t.kind == kTileStream) {
     constexpr int U = quad_unroll<Epi>() > 2 ? 2 : quad_unroll<Epi>();
     double* sprod = reinterpret_cast<double*>(smem);
@@ -251,7 +325,8 @@ __device__ void run_tile(const Tile& t, const int* __restrict__ rp, const int* _
       for (int j = 0; j < Epi::NA; ++j) acc[i][j] = 0.0;
       if (r < t.row1) {
         nvalid = i + 1;
-        const int a = rp[r] - t.k0, b = rp[r + 1] - t.k0;
+        const int a = t.part ? (r - t.row0) * t.part : rp[r] - t.k0;
+        const int b = t.part ? a + t.part : rp[r + 1] - t.k0;
         for (int s = a; s < b; ++s) {
           double p[Epi::NP];
 #pragma unroll

@@ -31,7 +31,12 @@ TilePlan plan_tiles(int64_t rows, const Off* rp, bool parity, int stream_max_row
       // end interior tiles on a multiple of 4 rows so the 4-row groups of the
       // next tile stay 32-byte aligned for vector epilogues
       if (r < brk && r - r0 > 4 && (r & 3) && len(r) <= stream_max_row) r -= (r & 3);
-      plan.tiles.push_back({kTileStream, int32_t(r0), int32_t(r), int32_t(k0), int32_t(rp[r]), 0, 1, 0});
+      // uniform row length L (every row of the tile): the kernels index rows as
+      // k0 + (r - row0) * L and skip the row offsets (Tile::part = L, else 0)
+      int32_t uni = r > r0 ? int32_t(len(r0)) : 0;
+      for (int64_t i = r0 + 1; i < r && uni > 0; ++i)
+        if (len(i) != uni) uni = 0;
+      plan.tiles.push_back({kTileStream, int32_t(r0), int32_t(r), int32_t(k0), int32_t(rp[r]), uni, 1, 0});
       ++plan.stream_tiles;
     } else if (!parity && l <= warp_max_row) {
       // lanes per row: ~lane_nnz per lane, a power of two in [8, threads]

@@ -30,7 +30,7 @@ struct Tile {
   int32_t row1;   // STREAM/WARP: end row; CHUNK: counter index of a split row (-1 if unsplit)
   int32_t k0;
   int32_t k1;
-  int32_t part;
+  int32_t part;   // WARP: lanes per row; CHUNK: slice index; STREAM: uniform row length (0 = mixed)
   int32_t nparts;
   int32_t slot;   // CHUNK: first partial slot of the row; WARP: 1 = element-interleaved lanes
 };

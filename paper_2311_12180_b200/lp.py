@@ -232,7 +232,7 @@ class SolverParams:
     device: int = 0
     mode: Mode = Mode.FAST
     use_cuda_graph: bool = True
-    l2_persist: bool = True
+    l2_persist: bool = False  # access-policy window on the gathered iterate (opt-in)
     engine: int = 0  # abi.ENGINE_*: AUTO = the CUDA-graph window (STREAM without graphs)
     # row sharding: rank `rank` of `world_size` (see ShardGroup)
     world_size: int = 1

@@ -92,13 +92,13 @@ def test_decision_kernel_variants_bitwise():
     (chosen by operator size) gives bitwise identical solves."""
     lp = generators.config("C1")
     out = []
-    for v in ("0", "1"):
+    for v in ("0", "1", "2"):
         os.environ["PDLP_DECIDE_SEP"] = v
         try:
             out.append(solve(lp, SolverParams(eps_optimal=1e-6)))
         finally:
             del os.environ["PDLP_DECIDE_SEP"]
-    assert same(out[0], out[1])
+    assert same(out[0], out[1]) and same(out[0], out[2])
 
 
 def test_sharded_repeat_solves_and_graph_engine_single_rank_equal():
