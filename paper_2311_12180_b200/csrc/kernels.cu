@@ -1025,7 +1025,7 @@ __global__ void gather_transpose_kernel(const int* perm, const int* row_of, cons
 // Planner input: does row r have mostly consecutive columns (and more than
 // min_len entries)? One warp per row.
 __global__ void row_contig_kernel(const int* rp, const int* col, int rows, int min_len,
-                                  unsigned char* out) {
+                                  int want_contig, unsigned char* out) {
   const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= rows) return;
@@ -1035,7 +1035,21 @@ __global__ void row_contig_kernel(const int* rp, const int* col, int rows, int m
     for (int k = k0 + lane; k + 1 < k1; k += 32) cnt += (col[k + 1] == col[k] + 1) ? 1 : 0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-  if (lane == 0) out[w] = (k1 - k0 > min_len && 2 * cnt >= k1 - k0 - 1) ? 1 : 0;
+  int flag = (k1 - k0 > min_len && 2 * cnt >= k1 - k0 - 1) ? 1 : 0;
+  if (!want_contig) flag = 0;
+  // 2: first row of four column-shifted rows (row w + i = row w's columns + i)
+  if ((w & 3) == 0 && w + 3 < rows && k1 - k0 > min_len) {
+    const int L = k1 - k0;
+    bool ok = rp[w + 4] - rp[w + 3] == L && rp[w + 3] - rp[w + 2] == L && rp[w + 2] - rp[w + 1] == L;
+    if (ok) {
+      int bad = 0;
+      for (int i = 1; i < 4; ++i)
+        for (int k = lane; k < L; k += 32) bad |= col[k0 + i * L + k] != col[k0 + k] + i;
+      ok = __any_sync(0xffffffffu, bad) == 0;
+    }
+    if (ok) flag = 2;
+  }
+  if (lane == 0) out[w] = (unsigned char)flag;
 }
 
 __global__ void fill_kernel(double* p, int64_t n, double v) {
@@ -1203,11 +1217,12 @@ void launch_gather_transpose(const int* perm, const int* row_of, const double* v
   gather_transpose_kernel<<<grid_for(nnz), kThreads, 0, s>>>(perm, row_of, val, nnz, col_t, val_t);
   PDLP_CUDA(cudaGetLastError());
 }
-void launch_row_contig(const int* rp, const int* col, int rows, int min_len, unsigned char* out,
-                       cudaStream_t s) {
+void launch_row_contig(const int* rp, const int* col, int rows, int min_len, int want_contig,
+                       unsigned char* out, cudaStream_t s) {
   const int64_t threads = int64_t(rows) * 32;
   const int64_t grid = (threads + kThreads - 1) / kThreads;
-  if (grid > 0) row_contig_kernel<<<unsigned(grid), kThreads, 0, s>>>(rp, col, rows, min_len, out);
+  if (grid > 0)
+    row_contig_kernel<<<unsigned(grid), kThreads, 0, s>>>(rp, col, rows, min_len, want_contig, out);
   PDLP_CUDA(cudaGetLastError());
 }
 void launch_fill(double* p, int64_t n, double v, cudaStream_t s) {

@@ -26,9 +26,10 @@ void launch_count_cols(const int* col, int64_t nnz, int* counts, cudaStream_t s)
 void launch_gather_transpose(const int* perm, const int* row_of, const double* val, int64_t nnz,
                              int* col_t, double* val_t, cudaStream_t s);
 void launch_fill(double* p, int64_t n, double v, cudaStream_t s);
-// out[r] = 1 when row r has more than min_len entries, mostly consecutive columns
-void launch_row_contig(const int* rp, const int* col, int rows, int min_len, unsigned char* out,
-                       cudaStream_t s);
+// Planner flags per row (more than min_len entries): 2 = first of four
+// column-shifted rows; 1 = mostly consecutive columns (when want_contig); 0 = neither
+void launch_row_contig(const int* rp, const int* col, int rows, int min_len, int want_contig,
+                       unsigned char* out, cudaStream_t s);
 void launch_fill_int(int* p, int64_t n, int v, cudaStream_t s);
 // Ruiz (scaling.hpp:52-66): out[r] = max_k |v_k * (d_row[r] * d_col[col_k])|
 void launch_row_absmax(const int* rp, const int* col, const double* val, int rows,

@@ -256,12 +256,13 @@ void Solver::setup(const pdlp_lp& lp) {
   std::vector<uint8_t> kcon, ktcon;
   const std::vector<uint8_t>* kc_p = nullptr;
   const std::vector<uint8_t>* ktc_p = nullptr;
-  // (measured on C2: -7% SpMV time over K but a different rounding trajectory;
-  // opt-in until the dual kernel's other costs shrink)
-  if (!parity() && std::getenv("PDLP_CONTIG")) {
+  // and groups of four column-shifted rows share one interleaved tile (the
+  // contiguous-row mode is opt-in: measured -7% SpMV time over K on C2)
+  if (!parity() && !std::getenv("PDLP_NO_ROW_GROUPS")) {
+    const int want_contig = std::getenv("PDLP_CONTIG") ? 1 : 0;
     DevBuf<unsigned char> f1{static_cast<size_t>(m_)}, f2{static_cast<size_t>(n_)};
-    launch_row_contig(k_rp_.get(), k_col_.get(), int(m_), kStreamMaxRow, f1.get(), s);
-    launch_row_contig(kt_rp_.get(), kt_col_.get(), int(n_), kStreamMaxRow, f2.get(), s);
+    launch_row_contig(k_rp_.get(), k_col_.get(), int(m_), kStreamMaxRow, want_contig, f1.get(), s);
+    launch_row_contig(kt_rp_.get(), kt_col_.get(), int(n_), kStreamMaxRow, want_contig, f2.get(), s);
     kcon.resize(size_t(m_));
     ktcon.resize(size_t(n_));
     if (m_) PDLP_CUDA(cudaMemcpyAsync(kcon.data(), f1.get(), size_t(m_), cudaMemcpyDeviceToHost, s));

@@ -337,6 +337,38 @@ __device__ void run_tile(const Tile& t, const int* __restrict__ rp, const int* _
     }
     epi.template rows_strided<RPT>(t.row0 + tid, kThreads, nvalid, acc, red);
     __syncthreads();
+  } else if (t.kind == kTileWarp && t.slot == 2 && !kSeq) {
+    // Four column-shifted rows (row r0 + i has the columns of row r0 shifted by
+    // +i, e.g. the demand rows of a transportation LP): thread t works on row
+    // t % 4, elements t / 4, t / 4 + 64, ...; the four lanes that share an
+    // element index gather x[c], x[c+1], x[c+2], x[c+3] from one 32-byte sector.
+    const int r = t.row0 + (tid & 3);
+    double acc[Epi::NA];
+    zero_acc<Epi>(acc);
+    elem_partial(epi, col, val, rp[r], rp[r + 1], tid >> 2, kThreads / 4, acc);
+    __shared__ double sgrp4[kWarps * 4 * Epi::NA];
+#pragma unroll
+    for (int i = 0; i < Epi::NA; ++i) {
+      double v = acc[i];
+      for (int o = 16; o >= 4; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);  // same row
+      acc[i] = v;
+    }
+    const int warp = tid >> 5, lane32 = tid & 31;
+    if (lane32 < 4) {
+#pragma unroll
+      for (int i = 0; i < Epi::NA; ++i) sgrp4[(warp * 4 + lane32) * Epi::NA + i] = acc[i];
+    }
+    __syncthreads();
+    if (tid < 4) {
+#pragma unroll
+      for (int i = 0; i < Epi::NA; ++i) {
+        double v = sgrp4[tid * Epi::NA + i];
+        for (int w = 1; w < kWarps; ++w) v += sgrp4[(w * 4 + tid) * Epi::NA + i];
+        acc[i] = v;
+      }
+      epi.row_done(t.row0 + tid, acc, red);
+    }
+    __syncthreads();
   } else if (t.kind == kTileWarp) {
     // G lanes per row (t.part in {8,...,256}, ~8 nnz per lane: one batch of
     // loads), kThreads / G rows per tile; lane partials combine by a fixed

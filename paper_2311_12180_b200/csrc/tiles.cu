@@ -14,7 +14,7 @@ TilePlan plan_tiles(int64_t rows, const Off* rp, bool parity, int stream_max_row
                     const std::vector<uint8_t>* contig) {
   // rows whose columns are mostly consecutive (contig[r] != 0) get
   // element-interleaved WARP tiles; others quad-strided ones
-  auto cflag = [&](int64_t i) { return contig && (*contig)[size_t(i)] ? 1 : 0; };
+  auto cflag = [&](int64_t i) { return contig ? int((*contig)[size_t(i)]) : 0; };
   TilePlan plan;
   int64_t r = 0;
   size_t bi = 0;
@@ -38,6 +38,13 @@ TilePlan plan_tiles(int64_t rows, const Off* rp, bool parity, int stream_max_row
         if (len(i) != uni) uni = 0;
       plan.tiles.push_back({kTileStream, int32_t(r0), int32_t(r), int32_t(k0), int32_t(rp[r]), uni, 1, 0});
       ++plan.stream_tiles;
+    } else if (!parity && l <= warp_max_row && contig && (*contig)[size_t(r)] == 2 && r + 4 <= brk) {
+      // four column-shifted rows in one interleaved tile (contig flag 2 marks
+      // the first row of such a group; spmv_engine.cuh)
+      plan.tiles.push_back({kTileWarp, int32_t(r), int32_t(r + 4), int32_t(rp[r]), int32_t(rp[r + 4]),
+                            threads / 4, 1, 2});
+      ++plan.warp_tiles;
+      r += 4;
     } else if (!parity && l <= warp_max_row) {
       // lanes per row: ~lane_nnz per lane, a power of two in [8, threads]
       auto lanes = [&](int64_t L) {
@@ -51,7 +58,8 @@ TilePlan plan_tiles(int64_t rows, const Off* rp, bool parity, int stream_max_row
       while (r < brk && r - r0 < threads / g && len(r) > stream_max_row && len(r) <= warp_max_row &&
              lanes(len(r)) == g && cflag(r) == cf)
         ++r;
-      plan.tiles.push_back({kTileWarp, int32_t(r0), int32_t(r), int32_t(rp[r0]), int32_t(rp[r]), g, 1, cf});
+      plan.tiles.push_back({kTileWarp, int32_t(r0), int32_t(r), int32_t(rp[r0]), int32_t(rp[r]), g, 1,
+                            cf == 1 ? 1 : 0});
       ++plan.warp_tiles;
     } else {
       const int64_t k0 = rp[r], k1 = rp[r + 1];
