@@ -310,6 +310,8 @@ def run_ours(args):
             "solve_1e-8": tol8,
             "time_to_tolerance_ms": 1e3 * last.info["device_seconds"], "iterations": last.iterations,
             "window_ms": 1e3 * last.info["window_seconds"], "eval_ms": 1e3 * last.info["eval_seconds"],
+            "host_gap_ms": 1e3 * (last.info["device_seconds"] - last.info["window_seconds"]
+                                  - last.info["eval_seconds"]),
             "restarts": last.restarts, "status": str(last.status),
             "primal_objective": last.info["primal_objective"],
             "setup_ms": 1e3 * last.info["setup_seconds"],

@@ -1038,7 +1038,9 @@ __global__ void row_contig_kernel(const int* rp, const int* col, int rows, int m
   int flag = (k1 - k0 > min_len && 2 * cnt >= k1 - k0 - 1) ? 1 : 0;
   if (!want_contig) flag = 0;
   // 2: first row of four column-shifted rows (row w + i = row w's columns + i)
-  if ((w & 3) == 0 && w + 3 < rows && k1 - k0 > min_len) {
+  // (only for rows long enough to give each of the group's 64 lanes per row
+  // several elements; short shifted rows stay in ordinary WARP tiles)
+  if ((w & 3) == 0 && w + 3 < rows && k1 - k0 >= 256) {
     const int L = k1 - k0;
     bool ok = rp[w + 4] - rp[w + 3] == L && rp[w + 3] - rp[w + 2] == L && rp[w + 2] - rp[w + 1] == L;
     if (ok) {
@@ -1359,7 +1361,7 @@ void launch_restart_copy(const DevIter& it, int from_avg, cudaStream_t s) {
 int eval_grid(int ntiles) { return ntiles; }  // one tile per CTA: short latency chains
 
 void launch_eval(const DevCsr& k, const DevCsr& kt, const DevIter& it, const DevEval& ev, bool seq,
-                 cudaStream_t s, const PhaseFn& phase) {
+                 cudaStream_t s, const PhaseFn& phase, const EvalFork* fork) {
   const int span = kThreads * kEv0Items;
   const int xblocks = ceil_div(it.n, span);
   if (it.world > 1) {  // the average slices to every rank, then the redundant EV0
@@ -1378,8 +1380,20 @@ void launch_eval(const DevCsr& k, const DevCsr& kt, const DevIter& it, const Dev
     eval_final_kernel<true><<<1, kThreads, 0, s>>>(ev, ev.ev1_tiles, ev.ev2_tiles, it.n, it.m, it.m1);
     eval_seq_displacement_kernel<<<1, 32, 0, s>>>(it, ev.out);
   } else {
-    eval_rows_kernel<false><<<g1, kThreads, sm1, s>>>(k, ev, it.m, it.m1);
-    eval_cols_kernel<false><<<g2, kThreads, sm2, s>>>(kt, ev, it.n, it.m1, -1);
+    if (fork && it.world == 1) {
+      // EV1 (rows of K) and EV2 (rows of K^T) are independent latency-bound
+      // passes over the same unscaled points: run them side by side
+      PDLP_CUDA(cudaEventRecord(fork->e_fork, s));
+      PDLP_CUDA(cudaStreamWaitEvent(fork->s2, fork->e_fork, 0));
+      eval_cols_kernel<false><<<g2, kThreads, sm2, fork->s2>>>(kt, ev, it.n, it.m1, -1);
+      PDLP_CUDA(cudaGetLastError());
+      PDLP_CUDA(cudaEventRecord(fork->e_join, fork->s2));
+      eval_rows_kernel<false><<<g1, kThreads, sm1, s>>>(k, ev, it.m, it.m1);
+      PDLP_CUDA(cudaStreamWaitEvent(s, fork->e_join, 0));
+    } else {
+      eval_rows_kernel<false><<<g1, kThreads, sm1, s>>>(k, ev, it.m, it.m1);
+      eval_cols_kernel<false><<<g2, kThreads, sm2, s>>>(kt, ev, it.n, it.m1, -1);
+    }
     PDLP_CUDA(cudaGetLastError());
     if (it.world > 1 && phase) phase();
     eval_final_kernel<false><<<1, kThreads, 0, s>>>(ev, ev.ev1_tiles, ev.ev2_tiles, it.n, it.m, it.m1);

@@ -67,8 +67,13 @@ void launch_zero_iterate(const DevIter& it, cudaStream_t s);
 void launch_restart_copy(const DevIter& it, int from_avg, cudaStream_t s);
 
 // ---- evaluation ------------------------------------------------------------
+// Side stream + events for running EV1 and EV2 concurrently (single device).
+struct EvalFork {
+  cudaStream_t s2;
+  cudaEvent_t e_fork, e_join;
+};
 void launch_eval(const DevCsr& k, const DevCsr& kt, const DevIter& it, const DevEval& ev,
-                 bool seq, cudaStream_t s, const PhaseFn& phase = {});
+                 bool seq, cudaStream_t s, const PhaseFn& phase = {}, const EvalFork* fork = nullptr);
 int eval_grid0(int n, int m);
 int eval_grid(int ntiles);
 // Reduced costs of one evaluated point (slot 0..3) into lam[slot] (finish only).

@@ -115,6 +115,11 @@ Solver::Solver(const pdlp_lp& lp, const pdlp_params& params) : params_(params) {
   validate_input(lp, params);
   PDLP_CUDA(cudaSetDevice(params.device));
   PDLP_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  if (!std::getenv("PDLP_NO_EVAL_FORK")) {
+    PDLP_CUDA(cudaStreamCreateWithFlags(&fork_.s2, cudaStreamNonBlocking));
+    PDLP_CUDA(cudaEventCreateWithFlags(&fork_.e_fork, cudaEventDisableTiming));
+    PDLP_CUDA(cudaEventCreateWithFlags(&fork_.e_join, cudaEventDisableTiming));
+  }
   setup(lp);
   PDLP_CUDA(cudaStreamSynchronize(stream_));
   setup_seconds_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - t).count();
@@ -127,6 +132,9 @@ Solver::~Solver() {
   if (ev_w0_) cudaEventDestroy(ev_w0_);
   if (ev_w1_) cudaEventDestroy(ev_w1_);
   if (ev_e1_) cudaEventDestroy(ev_e1_);
+  if (fork_.e_fork) cudaEventDestroy(fork_.e_fork);
+  if (fork_.e_join) cudaEventDestroy(fork_.e_join);
+  if (fork_.s2) cudaStreamDestroy(fork_.s2);
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
   if (graph_) cudaGraphDestroy(graph_);
   if (stream_) cudaStreamDestroy(stream_);
@@ -688,7 +696,17 @@ void Solver::upload_state() {
 void Solver::download_state() {
   PDLP_CUDA(cudaMemcpyAsync(hs_, state_dev_, sizeof(DevState), cudaMemcpyDeviceToHost,
                             stream_));
-  PDLP_CUDA(cudaStreamSynchronize(stream_));
+  spin_sync();
+}
+
+// The per-window round trip waits by polling the stream: the host resumes as
+// soon as the device finishes instead of after a blocking-sync wake-up.
+void Solver::spin_sync() {
+  for (;;) {
+    const cudaError_t e = cudaStreamQuery(stream_);
+    if (e == cudaSuccess) return;
+    if (e != cudaErrorNotReady) PDLP_CUDA(e);
+  }
 }
 
 double Solver::elapsed() const {
@@ -840,7 +858,7 @@ void Solver::run_window(int target) {
   PDLP_CUDA(cudaEventRecord(ev_w1_, stream_));
   // the evaluation block is enqueued behind the window (it reads the device
   // state), so one host round trip per window brings back state, scalars, log
-  launch_eval(k_ev_.csr, kt_ev_.csr, it_, ev_, parity(), stream_, phase_);
+  launch_eval(k_ev_.csr, kt_ev_.csr, it_, ev_, parity(), stream_, phase_, fork_.s2 ? &fork_ : nullptr);
   PDLP_CUDA(cudaEventRecord(ev_e1_, stream_));
   launches_ += parity() ? 5 : 4;
   ++evaluations_;
@@ -851,7 +869,7 @@ void Solver::run_window(int target) {
     PDLP_CUDA(cudaMemcpyAsync(log_host_.get(), step_log_dev_.get(),
                               size_t(target) * sizeof(pdlp_step_log_entry), cudaMemcpyDeviceToHost,
                               stream_));
-  PDLP_CUDA(cudaStreamSynchronize(stream_));
+  spin_sync();
   eval_fresh_ = true;
   {
     float ms = 0.f;
@@ -869,12 +887,12 @@ void Solver::run_window(int target) {
 void Solver::evaluate() {
   if (eval_fresh_) return;  // nothing changed since the window's own evaluation
   upload_state();
-  launch_eval(k_ev_.csr, kt_ev_.csr, it_, ev_, parity(), stream_, phase_);
+  launch_eval(k_ev_.csr, kt_ev_.csr, it_, ev_, parity(), stream_, phase_, fork_.s2 ? &fork_ : nullptr);
   launches_ += parity() ? 5 : 4;
   ++evaluations_;
   PDLP_CUDA(cudaMemcpyAsync(he_, eval_dev_, sizeof(EvalOut), cudaMemcpyDeviceToHost,
                             stream_));
-  PDLP_CUDA(cudaStreamSynchronize(stream_));
+  spin_sync();
   eval_fresh_ = true;
 }
 

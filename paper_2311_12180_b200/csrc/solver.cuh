@@ -164,6 +164,7 @@ class Solver {
   void capture_window_graph();
   void upload_state();
   void download_state();
+  void spin_sync();
   void run_window(int target);
   void evaluate();
   KktHost kkt(int slot) const;
@@ -230,6 +231,7 @@ class Solver {
   cudaEvent_t ev_begin_ = nullptr, ev_end_ = nullptr, ev_w0_ = nullptr, ev_w1_ = nullptr;
   double window_seconds_ = 0.0, eval_seconds_ = 0.0;
   cudaEvent_t ev_e1_ = nullptr;
+  EvalFork fork_{};  // side stream for the concurrent evaluation passes
   // persistent window engine
   int engine_ = PDLP_ENGINE_PERSISTENT;
   int win_grid_ = 0;

@@ -21,7 +21,10 @@ lp = generators.config(sys.argv[1] if len(sys.argv) > 1 else "C2")
 eng = int(os.environ.get("ENGINE", "2"))
 s = Solver(lp, SolverParams(engine=eng))
 r = s.solve()
-print("solve", r.iterations, r.info["device_seconds"], "window", r.info["window_seconds"], flush=True)
+r = s.solve()
+print("solve", r.iterations, r.info["device_seconds"], "window", r.info["window_seconds"], "eval",
+      r.info["eval_seconds"], "gap", r.info["device_seconds"] - r.info["window_seconds"] - r.info["eval_seconds"],
+      flush=True)
 for which, name in ((2, "spmv K"), (3, "spmv KT"), (0, "dual"), (1, "primal")):
     ms, by = s.time_kernel(which, 100)
     print(f"{name:8s} {ms*1e3:7.1f} us  {by/1e6:7.1f} MB  {by/ms/1e6:7.0f} GB/s", flush=True)
