@@ -1054,6 +1054,11 @@ __global__ void row_contig_kernel(const int* rp, const int* col, int rows, int m
   if (lane == 0) out[w] = (unsigned char)flag;
 }
 
+__global__ void extract_slot_kernel(const double* v4, int slot, int64_t n, double* out) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = v4[i * 4 + slot];
+}
+
 __global__ void fill_kernel(double* p, int64_t n, double v) {
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += stride) p[k] = v;
@@ -1225,6 +1230,10 @@ void launch_row_contig(const int* rp, const int* col, int rows, int min_len, int
   const int64_t grid = (threads + kThreads - 1) / kThreads;
   if (grid > 0)
     row_contig_kernel<<<unsigned(grid), kThreads, 0, s>>>(rp, col, rows, min_len, want_contig, out);
+  PDLP_CUDA(cudaGetLastError());
+}
+void launch_extract_slot(const double* v4, int slot, int64_t n, double* out, cudaStream_t s) {
+  extract_slot_kernel<<<grid_for(n), kThreads, 0, s>>>(v4, slot, n, out);
   PDLP_CUDA(cudaGetLastError());
 }
 void launch_fill(double* p, int64_t n, double v, cudaStream_t s) {

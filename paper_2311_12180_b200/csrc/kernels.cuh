@@ -26,6 +26,8 @@ void launch_count_cols(const int* col, int64_t nnz, int* counts, cudaStream_t s)
 void launch_gather_transpose(const int* perm, const int* row_of, const double* val, int64_t nnz,
                              int* col_t, double* val_t, cudaStream_t s);
 void launch_fill(double* p, int64_t n, double v, cudaStream_t s);
+// out[i] = v4[4 i + slot] (one point of an interleaved evaluation array)
+void launch_extract_slot(const double* v4, int slot, int64_t n, double* out, cudaStream_t s);
 // Planner flags per row (more than min_len entries): 2 = first of four
 // column-shifted rows; 1 = mostly consecutive columns (when want_contig); 0 = neither
 void launch_row_contig(const int* rp, const int* col, int rows, int min_len, int want_contig,

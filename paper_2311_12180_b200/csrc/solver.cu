@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -141,6 +142,17 @@ Solver::~Solver() {
 }
 
 void Solver::setup(const pdlp_lp& lp) {
+  // PDLP_TRACE_SETUP=1: per-phase wall times of the setup on stderr
+  const bool trace = std::getenv("PDLP_TRACE_SETUP") != nullptr;
+  auto tp = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!trace) return;
+    PDLP_CUDA(cudaStreamSynchronize(stream_));
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[pdlp setup] %-14s %8.2f ms\n", what,
+                 1e3 * std::chrono::duration<double>(now - tp).count());
+    tp = now;
+  };
   // validated by validate_input() before any device work
   const pdlp_csr& G = lp.inequality_matrix;
   const pdlp_csr& A = lp.equality_matrix;
@@ -212,7 +224,9 @@ void Solver::setup(const pdlp_lp& lp) {
   if (herr & 2) invalid("csr: row_offsets must be nondecreasing");
   if (herr & 4) invalid("csr: column indices must be strictly increasing within a row");
 
+  mark("upload");
   build_transpose();
+  mark("transpose");
 
   // original vectors on the device (evaluation on the unscaled LP)
   auto up = [&](DevBuf<double>& d, const std::vector<double>& h) {
@@ -227,6 +241,7 @@ void Solver::setup(const pdlp_lp& lp) {
   up(q_orig_, q_);
 
   precondition();
+  mark("precondition");
 
   // tile plans (host planner over the offsets)
   std::vector<int> rp_h(m_ + 1), rpt_h(n_ + 1);
@@ -260,6 +275,7 @@ void Solver::setup(const pdlp_lp& lp) {
   const int64_t c0 = world_ > 1 ? kt_cuts_[rank_] : 0, c1 = world_ > 1 ? kt_cuts_[rank_ + 1] : n_;
   // three tilings of each operator: iteration kernels, persistent window
   // kernel, evaluation kernels (common.cuh TileGeom)
+  mark("offsets");
   // rows with mostly consecutive columns get element-interleaved lane groups
   std::vector<uint8_t> kcon, ktcon;
   const std::vector<uint8_t>* kc_p = nullptr;
@@ -306,9 +322,12 @@ void Solver::setup(const pdlp_lp& lp) {
     plan_hash_ = h;
   }
 
+  mark("plans");
   allocate_iteration();
+  mark("allocate");
   set_kernel_attributes();
   pin_iterates_in_l2();
+  mark("attributes");
 }
 
 void Solver::build_plan(OpPlan& p, const DevCsr& base, const std::vector<int>& rp,
@@ -595,6 +614,7 @@ void Solver::allocate_iteration() {
   Y4_.alloc(size_t(m_) * 4);
   lam_.alloc(size_t(n_) * 4);
   scratch_n_.alloc(n_);
+  scratch_m_.alloc(m_);
   const int grid0 = eval_grid0(int(n_), int(m_));
   part0_.alloc(size_t(std::max(1, grid0)) * 4);
   const int ev1_tiles = int(k_ev_.plan.tiles.size()), ev2_tiles = int(kt_ev_.plan.tiles.size());
@@ -1013,24 +1033,29 @@ void Solver::finish(int status, int slot_x, int slot_y, int slot_lam, const KktH
   rx_.assign(n_, 0.0);
   ry_.assign(m_, 0.0);
   rlam_.assign(n_, 0.0);
-  if (slot_x >= 0 && n_)
-    PDLP_CUDA(cudaMemcpy2DAsync(rx_.data(), sizeof(double), X4_.get() + slot_x, 4 * sizeof(double),
-                                sizeof(double), n_, cudaMemcpyDeviceToHost, s));
-  if (slot_y >= 0 && m_)
-    PDLP_CUDA(cudaMemcpy2DAsync(ry_.data(), sizeof(double), Y4_.get() + slot_y, 4 * sizeof(double),
-                                sizeof(double), m_, cudaMemcpyDeviceToHost, s));
+  // the returned point is one slot of the interleaved [.][4] evaluation
+  // arrays: extract it on the device (a pitched 8-byte-wide D2H copy costs
+  // milliseconds at n = 1e6), then contiguous copies after the device clock
+  // stops (the solve's device time excludes the PCIe download)
+  const double* lam_src = nullptr;
+  if (slot_x >= 0 && n_) launch_extract_slot(X4_.get(), slot_x, n_, scratch_n_.get(), s);
+  if (slot_y >= 0 && m_) launch_extract_slot(Y4_.get(), slot_y, m_, scratch_m_.get(), s);
   if (n_) {
     if (slot_lam >= 0) {
       launch_eval_lambda(kt_ev_.csr, it_, ev_, parity(), slot_lam, s, phase_);
-      PDLP_CUDA(cudaMemcpyAsync(rlam_.data(), lam_.get() + size_t(slot_lam) * n_,
-                                n_ * sizeof(double), cudaMemcpyDeviceToHost, s));
-    } else {
-      launch_reduced_of_objective(c_orig_.get(), l_orig_.get(), u_orig_.get(), int(n_),
-                                  scratch_n_.get(), s);
-      PDLP_CUDA(cudaMemcpyAsync(rlam_.data(), scratch_n_.get(), n_ * sizeof(double),
-                                cudaMemcpyDeviceToHost, s));
+      lam_src = lam_.get() + size_t(slot_lam) * n_;
+    } else {  // reduced_costs(lp, 0) of a dual-infeasibility exit, into lam_'s slot 0
+      launch_reduced_of_objective(c_orig_.get(), l_orig_.get(), u_orig_.get(), int(n_), lam_.get(), s);
+      lam_src = lam_.get();
     }
   }
+  PDLP_CUDA(cudaEventRecord(ev_end_, s));
+  if (slot_x >= 0 && n_)
+    PDLP_CUDA(cudaMemcpyAsync(rx_.data(), scratch_n_.get(), n_ * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (slot_y >= 0 && m_)
+    PDLP_CUDA(cudaMemcpyAsync(ry_.data(), scratch_m_.get(), m_ * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (lam_src)
+    PDLP_CUDA(cudaMemcpyAsync(rlam_.data(), lam_src, n_ * sizeof(double), cudaMemcpyDeviceToHost, s));
   PDLP_CUDA(cudaStreamSynchronize(s));
   pdlp_result_info& in = info_;
   std::memset(&in, 0, sizeof in);
@@ -1051,8 +1076,6 @@ void Solver::finish(int status, int slot_x, int slot_y, int slot_lam, const KktH
   in.solve_seconds = elapsed();
   in.setup_seconds = setup_seconds_;
   {
-    PDLP_CUDA(cudaEventRecord(ev_end_, s));
-    PDLP_CUDA(cudaEventSynchronize(ev_end_));
     float ms = 0.f;
     PDLP_CUDA(cudaEventElapsedTime(&ms, ev_begin_, ev_end_));
     in.device_seconds = 1e-3 * double(ms);
