@@ -283,6 +283,18 @@ int pdlp_time_kernel(pdlp_handle* h, int32_t which, int32_t reps, double* avg_ms
 /* Problem sizes after create: {n, m, m1, nnz}. */
 int pdlp_get_sizes(pdlp_handle* h, int64_t* sizes);
 
+/* ---- CSR construction on the GPU --------------------------------------- */
+
+/* CsrMatrix::from_triplets (sparse_matrix.hpp:57-108) on device `device`:
+ * sorted by (row, col), duplicates summed in input order, exact zeros dropped.
+ * Outputs: row_offsets (rows + 1), col_indices / values (capacity nt);
+ * *nnz_out = stored entries. An out-of-range triplet returns PDLP_EINVAL with
+ * the reference's message naming the first one. Integer output is bit-exact
+ * with the reference; values too wherever a (row, col) occurs at most twice. */
+int pdlp_csr_from_triplets(int64_t rows, int64_t cols, int64_t nt, const int64_t* r, const int64_t* c,
+                           const double* v, int32_t device, int64_t* row_offsets, int64_t* col_indices,
+                           double* values, int64_t* nnz_out);
+
 /* ---- row sharding (B200 extension) ---------------------------------- */
 
 /* Size of one rank's exported shard blob. */

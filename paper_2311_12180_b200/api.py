@@ -68,6 +68,8 @@ def load_library(build_if_missing: bool = True) -> C.CDLL:
         "pdlp_lp_file_free": (None, [H]),
         "pdlp_write_solution": (C.c_int, [C.c_char_p, C.POINTER(abi.PdlpResultInfo), dp, C.c_int64, dp,
                                           C.c_int64]),
+        "pdlp_csr_from_triplets": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, i64p, i64p, dp, C.c_int32, i64p,
+                                             i64p, dp, i64p]),
         "pdlp_shard_blob_size": (C.c_int64, []),
         "pdlp_shard_link_local": (C.c_int, [C.POINTER(H), C.c_int32]),
         "pdlp_shard_export": (C.c_int, [H, C.c_void_p, C.c_int64]),
@@ -213,6 +215,22 @@ class Solver:
         ms, by = C.c_double(), C.c_double()
         _check(self._lib.pdlp_time_kernel(self._h, which, reps, C.byref(ms), C.byref(by)))
         return ms.value, by.value
+
+
+def csr_from_triplets(rows: int, cols: int, r, c, v, device: int = 0):
+    """CsrMatrix::from_triplets (sparse_matrix.hpp:57-108) on the GPU."""
+    from .lp import CsrMatrix
+
+    lib = load_library()
+    r = np.ascontiguousarray(r, dtype=np.int64)
+    c = np.ascontiguousarray(c, dtype=np.int64)
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    off, col, val = np.zeros(rows + 1, np.int64), np.zeros(r.size, np.int64), np.zeros(r.size)
+    nnz = C.c_int64()
+    _check(lib.pdlp_csr_from_triplets(rows, cols, r.size, abi.i64ptr(r), abi.i64ptr(c), abi.dptr(v), device,
+                                      abi.i64ptr(off), abi.i64ptr(col), abi.dptr(val), C.byref(nnz)))
+    k = nnz.value
+    return CsrMatrix(rows, cols, off, col[:k].copy(), val[:k].copy())
 
 
 def plan_shards(lp: GeneralFormLp, world: int) -> tuple[np.ndarray, np.ndarray]:
@@ -373,4 +391,5 @@ def solve(lp: GeneralFormLp, params: SolverParams | None = None) -> SolveResult:
 
 __all__ = ["Solver", "solve", "load_library", "default_params", "PdlpError", "library_path", "read_mps",
            "parse_mps", "write_solution", "MPS_FIXED", "MPS_FREE", "MPS_AUTO", "ShardGroup", "plan_shards",
+           "csr_from_triplets",
            "solve_distributed"]

@@ -314,3 +314,46 @@ def test_invalid_input_raises_value_error():
     bad.upper[1] = 1.0
     with pytest.raises(ValueError, match="empty bound interval on variable 1"):
         Solver(bad, SolverParams())
+
+
+# ---------------------------------------------------------------------------
+# GPU CSR construction (sparse_matrix.hpp:57-108)
+# ---------------------------------------------------------------------------
+
+def test_gpu_from_triplets_matches_oracle():
+    from paper_2311_12180_b200.api import csr_from_triplets
+
+    rng = np.random.default_rng(5)
+    for trial in range(30):
+        rows, cols = int(rng.integers(1, 300)), int(rng.integers(1, 300))
+        t = int(rng.integers(0, 3000))
+        r, c = rng.integers(0, rows, t), rng.integers(0, cols, t)
+        v = rng.uniform(-5, 5, t)
+        v[rng.uniform(size=t) < 0.05] = 0.0
+        if t > 4:  # exact cancellation of a duplicated pair: the entry is dropped
+            r[-1], c[-1], v[-1] = r[0], c[0], -v[0]
+        g = csr_from_triplets(rows, cols, r, c, v)
+        o = O.from_triplets(rows, cols, r, c, v)
+        assert np.array_equal(g.row_offsets, o.row_offsets)  # integer work: bit-exact
+        assert np.array_equal(g.col_indices, o.col_indices)
+        _, mult = np.unique(r * cols + c, return_counts=True)
+        if mult.max(initial=0) <= 2:
+            assert np.array_equal(g.values, o.values)
+        else:
+            assert np.allclose(g.values, o.values, rtol=1e-13, atol=1e-13)
+    with pytest.raises(ValueError, match="triplet 1 at \\(2, 0\\) is outside a 2x2 matrix"):
+        csr_from_triplets(2, 2, [0, 2, 5], [0, 0, 0], [1.0, 1.0, 1.0])
+    e = csr_from_triplets(3, 4, [], [], [])
+    assert list(e.row_offsets) == [0, 0, 0, 0] and e.nnz == 0
+
+
+def test_gpu_from_triplets_large_matches_host_csr():
+    from paper_2311_12180_b200.api import csr_from_triplets
+
+    lp = generators.config("C1")
+    K = stacked_k(lp)
+    rows = np.repeat(np.arange(K.num_rows), np.diff(K.row_offsets))
+    perm = np.random.default_rng(3).permutation(K.nnz)
+    g = csr_from_triplets(K.num_rows, K.num_cols, rows[perm], K.col_indices[perm], K.values[perm])
+    assert np.array_equal(g.row_offsets, K.row_offsets) and np.array_equal(g.col_indices, K.col_indices)
+    assert np.array_equal(g.values, K.values)

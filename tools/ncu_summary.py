@@ -103,12 +103,17 @@ def main() -> None:
         summary_path = prof / "ncu_summary.json"
         summary = json.loads(summary_path.read_text()) if summary_path.exists() else {}
         for name, lst in caps.items():
-            if lst and "dram_bytes_per_launch" in lst[0]:
-                summary[f"{name}_kernel"] = {
-                    "dram_bytes_per_launch": sum(d["dram_bytes_per_launch"] for d in lst) / len(lst),
-                    "time_us": sum(d.get("time", 0.0) for d in lst) / len(lst), "round": tag,
-                    "source": f"profiles/{tag}_ncu.json"}
-        summary_path.write_text(json.dumps(summary, indent=1))
+            by_kernel: dict = {}
+            for d in lst:
+                if "dram_bytes_per_launch" in d:
+                    base = d["kernel"].split("<")[0].split("::")[-1]
+                    by_kernel.setdefault(base, []).append(d)
+            for base, ds in by_kernel.items():
+                summary[base] = {
+                    "dram_bytes_per_launch": sum(d["dram_bytes_per_launch"] for d in ds) / len(ds),
+                    "time_us": sum(d.get("time", 0.0) for d in ds) / len(ds), "launches": len(ds),
+                    "capture": name, "round": tag, "source": f"profiles/{tag}_ncu.json"}
+        summary_path.write_text(json.dumps(summary, indent=1, sort_keys=True))
     print("wrote", sorted(p.name for p in prof.glob(f"{tag}_*")))
 
 
