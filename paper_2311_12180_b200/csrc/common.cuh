@@ -54,40 +54,32 @@ constexpr int kStreamRows = 2048;
 __host__ __device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }
 __host__ __device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }
 
-// Streaming loads of matrix data: read once per launch, so they bypass L1 and
-// are marked first-to-evict in L2, leaving L2 to the gathered iterate vector
-// (the random-access operand of every SpMV).
-__device__ __forceinline__ uint64_t l2_evict_first_policy() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
+// Streaming loads of matrix data: read once per launch, so they bypass L1.
+// (An L2 evict-first policy on them was measured: it evicts the operators that
+// stay L2-resident across iterations on C2-sized problems, 8.2 -> 20.5 us per
+// SpMV, and did not help the gather-bound C4 either.)
 __device__ __forceinline__ int4 ld_stream_i4(const int* p) {
   int4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p), "l"(l2_evict_first_policy()));
+               : "l"(p));
   return r;
 }
 __device__ __forceinline__ int ld_stream_i1(const int* p) {
   int r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
-               : "=r"(r)
-               : "l"(p), "l"(l2_evict_first_policy()));
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(r) : "l"(p));
   return r;
 }
 __device__ __forceinline__ double ld_stream_d1(const double* p) {
   double r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
-               : "=d"(r)
-               : "l"(p), "l"(l2_evict_first_policy()));
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
   return r;
 }
 __device__ __forceinline__ double2 ld_stream_d2(const double* p) {
   double2 r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
                : "=d"(r.x), "=d"(r.y)
-               : "l"(p), "l"(l2_evict_first_policy()));
+               : "l"(p));
   return r;
 }
 
@@ -100,7 +92,7 @@ __device__ __forceinline__ void griddep_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 __device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
 }
 
 // Fixed-order warp sum (xor butterfly): identical result on every replay.
