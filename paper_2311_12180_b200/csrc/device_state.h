@@ -60,6 +60,7 @@ struct EvalOut {
 // Row sharding across ranks (one rank per GPU)
 // ---------------------------------------------------------------------------
 constexpr int kMaxShards = 8;
+constexpr int kEvalReduceCtas = 32;  // first level of the evaluation reductions
 
 // Barrier kinds: each participating launch of a producer kernel bumps its
 // local count and publishes it to every peer's flag slot; a consumer waits
@@ -178,6 +179,7 @@ struct DevEval {
   double* seq_d;  // parity: [4][n] column residual terms
   EvalOut* out;
   int ev1_tiles, ev2_tiles;  // global evaluation tile counts (partials summed)
+  double* stage;             // [36][kEvalReduceCtas] first-level sums of the partials
   int world, rank;           // sharding (see DevIter)
   const ShardView* shv;
   ShardSync* sync;

@@ -831,17 +831,46 @@ __device__ double seq_dual_objective(const DevEval& ev, int slot, int n, int m) 
   return obj - ev.objective_constant;
 }
 
-template <bool kSeq>
-__global__ void __launch_bounds__(kThreads) eval_final_kernel(DevEval ev, int grid1, int grid2,
-                                                              int n, int m, int m1) {
-  double p0[4], p1[14], p2[18];
+// First level of the evaluation reductions: CTA g sums chunk g of each
+// partial array (fixed chunks, so the order is fixed) into ev.stage
+// ([36][kEvalReduceCtas], component-major).
+__global__ void __launch_bounds__(kThreads) eval_reduce_kernel(DevEval ev) {
   if (ev.world > 1) {
     shard_wait(ev.sync, ev.world, kSyncEvRows);
     shard_wait(ev.sync, ev.world, kSyncEvCols);
   }
-  sum_partials<4, 0>(ev.part0, ev.grid0, p0);
-  sum_partials<12, 2>(ev.part1, grid1, p1);
-  sum_partials<14, 4>(ev.part2, grid2, p2);
+  const int g = blockIdx.x, G = gridDim.x;
+  auto chunk = [&](int count, int& j0, int& j1) {
+    const int per = (count + G - 1) / G;
+    j0 = min(count, g * per);
+    j1 = min(count, j0 + per);
+  };
+  int a, b;
+  double p0[4], p1[14], p2[18];
+  chunk(ev.grid0, a, b);
+  sum_partials_range<4, 0>(ev.part0, ev.grid0, a, b, p0);
+  chunk(ev.ev1_tiles, a, b);
+  sum_partials_range<12, 2>(ev.part1, ev.ev1_tiles, a, b, p1);
+  chunk(ev.ev2_tiles, a, b);
+  sum_partials_range<14, 4>(ev.part2, ev.ev2_tiles, a, b, p2);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 4; ++i) ev.stage[i * G + g] = p0[i];
+    for (int i = 0; i < 14; ++i) ev.stage[(4 + i) * G + g] = p1[i];
+    for (int i = 0; i < 18; ++i) ev.stage[(18 + i) * G + g] = p2[i];
+  }
+}
+
+template <bool kSeq>
+__global__ void __launch_bounds__(kThreads) eval_final_kernel(DevEval ev, int grid1, int grid2,
+                                                              int n, int m, int m1) {
+  // the partial arrays were pre-reduced by kEvalReduceCtas CTAs of
+  // eval_reduce_kernel (fixed chunks); sum their chunk results in order
+  double p0[4], p1[14], p2[18];
+  sum_partials<4, 0>(ev.stage, kEvalReduceCtas, p0);
+  sum_partials<12, 2>(ev.stage + 4 * kEvalReduceCtas, kEvalReduceCtas, p1);
+  sum_partials<14, 4>(ev.stage + 18 * kEvalReduceCtas, kEvalReduceCtas, p2);
+  (void)grid1;
+  (void)grid2;
   EvalOut* o = ev.out;
   const double c0 = ev.objective_constant;
   if (threadIdx.x == 0) {
@@ -1386,6 +1415,7 @@ void launch_eval(const DevCsr& k, const DevCsr& kt, const DevIter& it, const Dev
   if (seq) {
     eval_rows_kernel<true><<<g1, kThreads, sm1, s>>>(k, ev, it.m, it.m1);
     eval_cols_kernel<true><<<g2, kThreads, sm2, s>>>(kt, ev, it.n, it.m1, -1);
+    eval_reduce_kernel<<<kEvalReduceCtas, kThreads, 0, s>>>(ev);
     eval_final_kernel<true><<<1, kThreads, 0, s>>>(ev, ev.ev1_tiles, ev.ev2_tiles, it.n, it.m, it.m1);
     eval_seq_displacement_kernel<<<1, 32, 0, s>>>(it, ev.out);
   } else {
@@ -1405,6 +1435,7 @@ void launch_eval(const DevCsr& k, const DevCsr& kt, const DevIter& it, const Dev
     }
     PDLP_CUDA(cudaGetLastError());
     if (it.world > 1 && phase) phase();
+    eval_reduce_kernel<<<kEvalReduceCtas, kThreads, 0, s>>>(ev);
     eval_final_kernel<false><<<1, kThreads, 0, s>>>(ev, ev.ev1_tiles, ev.ev2_tiles, it.n, it.m, it.m1);
   }
   PDLP_CUDA(cudaGetLastError());

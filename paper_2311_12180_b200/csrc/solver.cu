@@ -643,6 +643,8 @@ void Solver::allocate_iteration() {
   ev.out = eval_dev_;
   ev.ev1_tiles = ev1_tiles;
   ev.ev2_tiles = ev2_tiles;
+  eval_stage_.alloc(36 * size_t(kEvalReduceCtas));
+  ev.stage = eval_stage_.get();
 
   // sharding: own slices, sync block, peer table (own entries until linked)
   sync_.alloc(1);
@@ -880,7 +882,7 @@ void Solver::run_window(int target) {
   // state), so one host round trip per window brings back state, scalars, log
   launch_eval(k_ev_.csr, kt_ev_.csr, it_, ev_, parity(), stream_, phase_, fork_.s2 ? &fork_ : nullptr);
   PDLP_CUDA(cudaEventRecord(ev_e1_, stream_));
-  launches_ += parity() ? 5 : 4;
+  launches_ += parity() ? 6 : 5;  // prep, rows, cols, reduce, final (+ parity displacement)
   ++evaluations_;
   // evaluation results + state in one D2H copy
   PDLP_CUDA(cudaMemcpyAsync(he_, eval_dev_, xo_state_ + sizeof(DevState), cudaMemcpyDeviceToHost,
@@ -908,7 +910,7 @@ void Solver::evaluate() {
   if (eval_fresh_) return;  // nothing changed since the window's own evaluation
   upload_state();
   launch_eval(k_ev_.csr, kt_ev_.csr, it_, ev_, parity(), stream_, phase_, fork_.s2 ? &fork_ : nullptr);
-  launches_ += parity() ? 5 : 4;
+  launches_ += parity() ? 6 : 5;  // prep, rows, cols, reduce, final (+ parity displacement)
   ++evaluations_;
   PDLP_CUDA(cudaMemcpyAsync(he_, eval_dev_, sizeof(EvalOut), cudaMemcpyDeviceToHost,
                             stream_));

@@ -206,6 +206,7 @@ class Solver {
   DevBuf<pdlp_step_log_entry> step_log_dev_;
   DevState* state_dev_ = nullptr;  // inside xfer_dev_
   DevBuf<DevState> snap_dev_;
+  DevBuf<double> eval_stage_;
   DevBuf<double> X4_, Y4_, lam_, part0_, part1_, part2_, seq_r_, seq_d_, scratch_n_, scratch_m_;
   EvalOut* eval_dev_ = nullptr;  // inside xfer_dev_
   DevIter it_{};

@@ -316,26 +316,47 @@ __device__ void run_tile(const Tile& t, const int* __restrict__ rp, const int* _
     // and neighbouring epilogue operands from HBM (coalesced); each row is
     // summed in index order
     constexpr int RPT = Epi::kGeom.stream_rows / kThreads;
-    double acc[RPT][Epi::NA];
-    int nvalid = 0;
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-      const int r = t.row0 + tid + i * kThreads;
-#pragma unroll
-      for (int j = 0; j < Epi::NA; ++j) acc[i][j] = 0.0;
-      if (r < t.row1) {
-        nvalid = i + 1;
+    if constexpr (Epi::NA > 2) {
+      // wide accumulators (the evaluation epilogues carry 4-8 sums per row):
+      // finish each row before the next so only one row's sums are live
+#pragma unroll 1
+      for (int i = 0; i < RPT; ++i) {
+        const int r = t.row0 + tid + i * kThreads;
+        if (r >= t.row1) break;
+        double acc1[Epi::NA];
+        zero_acc<Epi>(acc1);
         const int a = t.part ? (r - t.row0) * t.part : rp[r] - t.k0;
         const int b = t.part ? a + t.part : rp[r + 1] - t.k0;
         for (int s = a; s < b; ++s) {
           double p[Epi::NP];
 #pragma unroll
           for (int j = 0; j < Epi::NP; ++j) p[j] = sprod[size_t(s) * Epi::NP + j];
-          epi.add(acc[i], p, Epi::kNeedCol ? scol[s] : 0);
+          epi.add(acc1, p, Epi::kNeedCol ? scol[s] : 0);
+        }
+        epi.row_done(r, acc1, red);
+      }
+    } else {
+      double acc[RPT][Epi::NA];
+      int nvalid = 0;
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const int r = t.row0 + tid + i * kThreads;
+#pragma unroll
+        for (int j = 0; j < Epi::NA; ++j) acc[i][j] = 0.0;
+        if (r < t.row1) {
+          nvalid = i + 1;
+          const int a = t.part ? (r - t.row0) * t.part : rp[r] - t.k0;
+          const int b = t.part ? a + t.part : rp[r + 1] - t.k0;
+          for (int s = a; s < b; ++s) {
+            double p[Epi::NP];
+#pragma unroll
+            for (int j = 0; j < Epi::NP; ++j) p[j] = sprod[size_t(s) * Epi::NP + j];
+            epi.add(acc[i], p, Epi::kNeedCol ? scol[s] : 0);
+          }
         }
       }
+      epi.template rows_strided<RPT>(t.row0 + tid, kThreads, nvalid, acc, red);
     }
-    epi.template rows_strided<RPT>(t.row0 + tid, kThreads, nvalid, acc, red);
     __syncthreads();
   } else if (t.kind == kTileWarp && t.slot == 2 && !kSeq) {
     // Four column-shifted rows (row r0 + i has the columns of row r0 shifted by
@@ -486,23 +507,24 @@ __device__ __forceinline__ bool grid_last_block(unsigned* counter, unsigned tota
   return is_last;
 }
 
-// Fixed-order reduction of `count` component-major partials of width NS+NM
-// (single CTA); the result is valid in thread 0.
+// Fixed-order reduction of the partials [j0, j1) of a component-major array
+// with row stride `stride` (single CTA); the result is valid in thread 0.
 template <int NS, int NM>
-__device__ __forceinline__ void sum_partials(const double* partials, int count, double (&out)[NS + NM]) {
+__device__ __forceinline__ void sum_partials_range(const double* partials, int stride, int j0, int j1,
+                                                   double (&out)[NS + NM]) {
   constexpr int K = NS + NM;
   constexpr int B = K <= 4 ? 8 : 2;  // loads in flight per thread
   __shared__ double sred[kWarps * K];
 #pragma unroll
   for (int i = 0; i < K; ++i) out[i] = i < NS ? 0.0 : -INFINITY;
-  for (int j0 = threadIdx.x; j0 < count; j0 += kThreads * B) {
+  for (int jb = j0 + threadIdx.x; jb < j1; jb += kThreads * B) {
     double v[B][K];
 #pragma unroll
     for (int b = 0; b < B; ++b) {
-      const int j = j0 + b * kThreads;
+      const int j = jb + b * kThreads;
 #pragma unroll
       for (int i = 0; i < K; ++i)
-        v[b][i] = j < count ? __ldcg(partials + size_t(i) * count + j) : (i < NS ? 0.0 : -INFINITY);
+        v[b][i] = j < j1 ? __ldcg(partials + size_t(i) * stride + j) : (i < NS ? 0.0 : -INFINITY);
     }
 #pragma unroll
     for (int b = 0; b < B; ++b) {
@@ -511,6 +533,12 @@ __device__ __forceinline__ void sum_partials(const double* partials, int count, 
     }
   }
   block_reduce<NS, NM>(out, sred);
+}
+
+// All `count` partials of a component-major array of width NS+NM.
+template <int NS, int NM>
+__device__ __forceinline__ void sum_partials(const double* partials, int count, double (&out)[NS + NM]) {
+  sum_partials_range<NS, NM>(partials, count, 0, count, out);
 }
 
 }  // namespace pdlp
