@@ -84,6 +84,18 @@ void launch_eval_lambda(const DevCsr& kt, const DevIter& it, const DevEval& ev, 
 void launch_reduced_of_objective(const double* c, const double* l, const double* u, int n,
                                  double* lam, cudaStream_t s);
 
+// ---- column panels (panels.cu) ---------------------------------------------
+void launch_panel_keys(const int* row_of, const int* col, int64_t nnz, int width, int rows, int* keys,
+                       cudaStream_t s);
+void launch_panel_gather(const int* perm, const int* col, const double* val, int64_t nnz, int* col_p,
+                         double* val_p, cudaStream_t s);
+void launch_panel_spread(const int* rp, const int* col, int rows, int width, unsigned long long* distinct,
+                         cudaStream_t s);
+int panel_combine_blocks(int rows);
+void launch_panel_dual(const DevCsr& kp, int panels, double* partial, const DevIter& it, cudaStream_t s);
+void launch_panel_primal(const DevCsr& ktp, int panels, double* partial, const DevIter& it, int mode_override,
+                         cudaStream_t s);
+
 void set_kernel_attributes();
 
 }  // namespace pdlp

@@ -322,12 +322,102 @@ void Solver::setup(const pdlp_lp& lp) {
     plan_hash_ = h;
   }
 
+  // column panels for operators that scatter over a vector much larger than
+  // L2 (fast mode, one device; panels.cu)
+  if (!parity() && world_ == 1 && !(std::getenv("PDLP_PANELS") && std::atoi(std::getenv("PDLP_PANELS")) == 0)) {
+    build_panels(kpan_, kpan_plan_, K_, int(m_), int(n_), "K");
+    build_panels(ktpan_, ktpan_plan_, KT_, int(n_), int(m_), "KT");
+  }
   mark("plans");
   allocate_iteration();
   mark("allocate");
   set_kernel_attributes();
   pin_iterates_in_l2();
   mark("attributes");
+}
+
+// Decides whether `op` (rows x cols) gets column panels and builds them: the
+// gathered vector must exceed the L2 budget (48 MB per panel) and the rows must
+// scatter over it (on average across at least half of min(panels, row length)
+// panels, i.e. no locality a single pass could use). PDLP_PANELS=1 forces
+// panels of PDLP_PANEL_WIDTH columns (tests); =0 disables them.
+void Solver::build_panels(PanelOp& po, OpPlan& plan, const DevCsr& op, int rows, int cols,
+                          const char* which) {
+  cudaStream_t s = stream_;
+  const char* force = std::getenv("PDLP_PANELS");
+  const bool forced = force && std::atoi(force) == 1;
+  int width = int(std::max<int64_t>(1, (int64_t(48) << 20) / 8));
+  if (forced && std::getenv("PDLP_PANEL_WIDTH")) width = std::max(1, std::atoi(std::getenv("PDLP_PANEL_WIDTH")));
+  const int panels = int((int64_t(cols) + width - 1) / width);
+  if (panels < 2 || rows < 1 || op.nnz < 1) return;
+  if (int64_t(panels) * rows >= int64_t(std::numeric_limits<int32_t>::max()) - 1024) return;
+  if (!forced) {
+    DevBuf<unsigned long long> d{static_cast<size_t>(1)};
+    d.zero(s);
+    launch_panel_spread(op.rp, op.col, rows, width, d.get(), s);
+    unsigned long long distinct = 0;
+    PDLP_CUDA(cudaMemcpyAsync(&distinct, d.get(), 8, cudaMemcpyDeviceToHost, s));
+    PDLP_CUDA(cudaStreamSynchronize(s));
+    const double per_row = double(distinct) / double(rows);
+    const double avg_len = double(op.nnz) / double(rows);
+    if (per_row < 0.5 * std::min(double(panels), avg_len)) return;
+  }
+  // stacked CSR: entry k of row r, column c goes to stacked row (c / width) * rows + r;
+  // a stable radix sort keeps each row's columns in increasing order
+  const int64_t nnz = op.nnz;
+  const int srows = panels * rows;
+  DevBuf<int> row_of{static_cast<size_t>(nnz)}, keys{static_cast<size_t>(nnz)},
+      keys2{static_cast<size_t>(nnz)}, ids{static_cast<size_t>(nnz)}, perm{static_cast<size_t>(nnz)},
+      counts{static_cast<size_t>(srows) + 1};
+  launch_expand_rows(op.rp, rows, row_of.get(), s);
+  launch_panel_keys(row_of.get(), op.col, nnz, width, rows, keys.get(), s);
+  launch_iota(ids.get(), nnz, s);
+  int end_bit = 1;
+  while ((int64_t(1) << end_bit) < srows) ++end_bit;
+  size_t tmp_bytes = 0;
+  PDLP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys.get(), keys2.get(), ids.get(), perm.get(),
+                                            int(nnz), 0, end_bit, s));
+  DevBuf<unsigned char> tmp{tmp_bytes};
+  PDLP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tmp_bytes, keys.get(), keys2.get(), ids.get(), perm.get(),
+                                            int(nnz), 0, end_bit, s));
+  counts.zero(s);
+  launch_count_cols(keys.get(), nnz, counts.get(), s);
+  po.rp.alloc(size_t(srows) + 1 + kVecPad);
+  po.rp.zero(s);
+  size_t scan_bytes = 0;
+  PDLP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, counts.get(), po.rp.get(), srows + 1, s));
+  DevBuf<unsigned char> scan_tmp{scan_bytes};
+  PDLP_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp.get(), scan_bytes, counts.get(), po.rp.get(), srows + 1, s));
+  po.col.alloc(size_t(nnz) + kVecPad);
+  po.val.alloc(size_t(nnz) + kVecPad);
+  po.col.zero(s);
+  po.val.zero(s);
+  launch_panel_gather(perm.get(), op.col, op.val, nnz, po.col.get(), po.val.get(), s);
+  std::vector<int> rp_h(size_t(srows) + 1);
+  PDLP_CUDA(cudaMemcpyAsync(rp_h.data(), po.rp.get(), rp_h.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
+  PDLP_CUDA(cudaStreamSynchronize(s));
+  const DevCsr base{po.rp.get(), po.col.get(), po.val.get(), nullptr, srows, cols, nnz};
+  build_plan(plan, base, rp_h, kIterGeom, {}, 0, srows);
+  po.partial.alloc(size_t(srows));
+  po.panels = panels;
+  po.width = width;
+  if (std::getenv("PDLP_TRACE_SETUP"))
+    std::fprintf(stderr, "[pdlp setup] %s: %d column panels of %d, %d tiles\n", which, panels, width,
+                 plan.csr.ntiles);
+}
+
+void Solver::dual_step(unsigned long long cond, int use_cond) {
+  if (kpan_.panels)
+    launch_panel_dual(kpan_plan_.csr, kpan_.panels, kpan_.partial.get(), it_, stream_);
+  else
+    launch_dual(K_, it_, parity(), cond, use_cond, stream_);
+}
+
+void Solver::primal_step(int mode_override, unsigned long long cond, int use_cond) {
+  if (ktpan_.panels)
+    launch_panel_primal(ktpan_plan_.csr, ktpan_.panels, ktpan_.partial.get(), it_, mode_override, stream_);
+  else
+    launch_primal(KT_, it_, parity(), mode_override, stream_, cond, use_cond);
 }
 
 void Solver::build_plan(OpPlan& p, const DevCsr& base, const std::vector<int>& rp,
@@ -510,7 +600,10 @@ void Solver::allocate_iteration() {
   const int64_t col0 = kt_cuts_[rank_], col1 = kt_cuts_[rank_ + 1];
   const int avg_blocks = std::max<int64_t>(1, (row1 - row0 + 4095) / 4096);
   const int p_grid = KT_.ntiles + avg_blocks;
-  const int k_tiles = int(k_it_.plan.tiles.size()), kt_tiles = int(kt_it_.plan.tiles.size());
+  // partial counts: one per tile of the operator's kernel, or one per combine
+  // block when the operator runs as column panels
+  const int k_tiles = kpan_.panels ? panel_combine_blocks(int(m_)) : int(k_it_.plan.tiles.size());
+  const int kt_tiles = ktpan_.panels ? panel_combine_blocks(int(n_)) : int(kt_it_.plan.tiles.size());
   d_part_.alloc(size_t(k_tiles) * 3);
   p_part_.alloc(size_t(kt_tiles) * 4 + 2);  // two parity buffers + dx^2 total
   p_part_.zero(s);
@@ -584,6 +677,8 @@ void Solver::allocate_iteration() {
   if (const char* e = std::getenv("PDLP_DECIDE_SEP")) it.decide_sep = parity() ? 0 : std::atoi(e);
   // 2 (decision in the dual's last CTA) needs every partial on this device
   if (world_ > 1 && it.decide_sep == 2) it.decide_sep = 1;
+  // panel kernels read the committed decision
+  if (kpan_.panels || ktpan_.panels) it.decide_sep = 1;
   it.seq_dy2 = seq_dy2_.get();
   it.seq_inter = seq_inter_.get();
   it.seq_dx2 = seq_dx2_.get();
@@ -702,9 +797,9 @@ void Solver::capture_window_graph() {
   const unsigned long long ch = static_cast<unsigned long long>(h);
   // whichever kernel takes the step decision sets the WHILE condition
   const int ds = it_.decide_sep;
-  launch_dual(K_, it_, parity(), ch, (parity() || ds == 2) ? 1 : 0, stream_);
+  dual_step(ch, (parity() || ds == 2) ? 1 : 0);
   if (ds == 1) launch_decide(it_, stream_, ch, 1);
-  launch_primal(KT_, it_, parity(), -1, stream_, ch, (!parity() && ds == 0) ? 1 : 0);
+  primal_step(-1, ch, (!parity() && ds == 0) ? 1 : 0);
   PDLP_CUDA(cudaStreamEndCapture(stream_, &body));
   PDLP_CUDA(cudaGraphInstantiate(&graph_exec_, graph_, 0));
   cond_handle_ = static_cast<unsigned long long>(h);
@@ -785,7 +880,7 @@ void Solver::iterate_begin(int32_t* status) {
   } else {
     // first trial x' = proj(x - tau (c - K'y)) at z = 0
     upload_state();
-    launch_primal(KT_, it_, parity(), kPRetry, stream_);
+    primal_step(kPRetry);
     phase();
     ++launches_;
     p_from_window_ = false;
@@ -866,10 +961,10 @@ void Solver::run_window(int target) {
     int remaining = target;
     while (true) {
       for (int i = 0; i < remaining; ++i) {
-        launch_dual(K_, it_, parity(), 0, 0, stream_);
+        dual_step(0, 0);
         phase();
         if (it_.decide_sep == 1) launch_decide(it_, stream_);
-        launch_primal(KT_, it_, parity(), -1, stream_);
+        primal_step(-1);
         phase();
       }
       download_state();
@@ -1007,7 +1102,7 @@ void Solver::evaluation_block() {
   outer_ += 1;
   upload_state();
   launch_spmv(K_, false, it_.x[st.ix_cur], it_.kx[st.ikx_cur], parity(), stream_);
-  launch_primal(KT_, it_, parity(), kPRestart, stream_);
+  primal_step(kPRestart);
   phase();
   launches_ += 3;
   eval_fresh_ = false;
@@ -1231,16 +1326,16 @@ void Solver::time_kernel(int which, int reps, double* avg_ms, double* bytes) {
   PDLP_CUDA(cudaMemcpyAsync(state_dev_, hs_, xo_tab_ - xo_state_ + 2 * sizeof(double) * size_t(reps),
                             cudaMemcpyHostToDevice, stream_));
   // a trial needs a fresh x'; recompute it from the current point
-  launch_primal(KT_, it_, parity(), kPRetry, stream_);
+  primal_step(kPRetry);
   std::vector<cudaEvent_t> ev(2 * reps);
   for (auto& e : ev) PDLP_CUDA(cudaEventCreate(&e));
   for (int r = 0; r < reps; ++r) {
     if (which == 0) PDLP_CUDA(cudaEventRecord(ev[2 * r], stream_));
-    launch_dual(K_, it_, parity(), 0, 0, stream_);
+    dual_step(0, 0);
     if (it_.decide_sep == 1) launch_decide(it_, stream_);
     if (which == 0) PDLP_CUDA(cudaEventRecord(ev[2 * r + 1], stream_));
     if (which == 1) PDLP_CUDA(cudaEventRecord(ev[2 * r], stream_));
-    launch_primal(KT_, it_, parity(), -1, stream_);
+    primal_step(-1);
     if (which == 1) PDLP_CUDA(cudaEventRecord(ev[2 * r + 1], stream_));
   }
   PDLP_CUDA(cudaStreamSynchronize(stream_));

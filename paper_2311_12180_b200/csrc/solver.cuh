@@ -155,6 +155,17 @@ class Solver {
                   const std::vector<int64_t>& breaks, int64_t r0, int64_t r1,
                   const std::vector<uint8_t>* contig = nullptr);
   void shard_view_upload();
+  // column panels of one operator (panels.cu): stacked CSR, its plan, partials
+  struct PanelOp {
+    int panels = 0;  // 0: not panelized
+    int width = 0;
+    DevBuf<int> rp, col;
+    DevBuf<double> val;
+    DevBuf<double> partial;  // [panels][rows]
+  };
+  void build_panels(PanelOp& po, OpPlan& plan, const DevCsr& op, int rows, int cols, const char* which);
+  void dual_step(unsigned long long cond, int use_cond);
+  void primal_step(int mode_override, unsigned long long cond = 0, int use_cond = 0);
   void phase() {
     if (phase_) phase_();
   }
@@ -190,6 +201,8 @@ class Solver {
   DevBuf<int> k_rp_, k_col_, kt_rp_, kt_col_;
   DevBuf<double> k_val_, k_val_orig_, kt_val_, kt_val_orig_;
   OpPlan k_it_, kt_it_, k_win_, kt_win_, k_ev_, kt_ev_;
+  PanelOp kpan_, ktpan_;
+  OpPlan kpan_plan_, ktpan_plan_;
   DevCsr K_{}, KT_{};  // the iteration-kernel tilings (this rank's tiles)
   DevCsr K_full_{}, KT_full_{};  // every tile (kernel-level API on a sharded rank)
 

@@ -357,3 +357,34 @@ def test_gpu_from_triplets_large_matches_host_csr():
     g = csr_from_triplets(K.num_rows, K.num_cols, rows[perm], K.col_indices[perm], K.values[perm])
     assert np.array_equal(g.row_offsets, K.row_offsets) and np.array_equal(g.col_indices, K.col_indices)
     assert np.array_equal(g.values, K.values)
+
+
+# ---------------------------------------------------------------------------
+# column panels (panels.cu): forced on small instances with narrow panels
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("which", ["C1", "transport", "skewed"])
+def test_column_panels_match_oracle(which, monkeypatch):
+    monkeypatch.setenv("PDLP_PANELS", "1")
+    monkeypatch.setenv("PDLP_PANEL_WIDTH", "700")
+    lp = {"C1": lambda: generators.config("C1"), "transport": lambda: generators.transport_lp(60, 80, seed=11),
+          "skewed": skewed_lp}[which]()
+    ref = O.Session(lp, SolverParams(), "oracle")
+    with Solver(lp, SolverParams()) as s:
+        s.iterate_begin()
+        worst = 0.0
+        for k in range(100):
+            s.iterate_run(1)
+            ref.run(1)
+            a, b = s.iterate(), ref.iterate()
+            assert (a["total"], a["inner"]) == (b["total"], b["inner"])
+            za, zb = np.concatenate([a["x"], a["y"]]), np.concatenate([b["x"], b["y"]])
+            worst = max(worst, float(np.linalg.norm(za - zb) / max(np.linalg.norm(zb), 1e-300)))
+    ref.close()
+    assert worst <= 1e-10, worst
+    p = SolverParams(eps_optimal=1e-6, iteration_limit=200000)
+    r, o = solve(lp, p), O.solve(lp, p)
+    assert r.status == o.status
+    if r.status == SolveStatus.OPTIMAL:
+        assert abs(r.info["primal_objective"] - o.info["primal_objective"]) <= 1e-5 * (
+            1.0 + abs(o.info["primal_objective"]))

@@ -8,7 +8,8 @@ from paper_2311_12180_b200 import Solver, SolverParams, generators
 
 which = sys.argv[1] if len(sys.argv) > 1 else "C2"
 lp = generators.config(which)
-s = Solver(lp, SolverParams(use_cuda_graph=os.environ.get("PDLP_GRAPH", "0") == "1"))
+limit = int(os.environ.get("PDLP_ITER_LIMIT", str(2**62)))
+s = Solver(lp, SolverParams(use_cuda_graph=os.environ.get("PDLP_GRAPH", "0") == "1", iteration_limit=limit))
 r = s.solve()
 print(which, r.status, r.iterations, r.info["device_seconds"])
 s.close()
