@@ -44,6 +44,9 @@ struct TileGeom {
 constexpr TileGeom kIterGeom{4096, 1024, 16, 4096};
 constexpr TileGeom kWinGeom{2048, 1024, 8, 2048};
 constexpr TileGeom kEvalGeom{1024, 1024, 8, 2048};
+// column-panel passes: stacked rows hold ~nnz/row/panels entries, so tiles take
+// up to 4096 rows (16 per thread) to keep ~4k nonzeros per CTA
+constexpr TileGeom kPanelGeom{4096, 4096, 16, 4096};
 constexpr int kStreamNnz = 4096;     // largest STREAM tile of any geometry
 constexpr int kStreamRows = 2048;
 
@@ -80,6 +83,51 @@ __device__ __forceinline__ double2 ld_stream_d2(const double* p) {
   asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
                : "=d"(r.x), "=d"(r.y)
                : "l"(p));
+  return r;
+}
+
+// Variants with an L2 evict-first cache policy, for matrix streams that will
+// not be reused from L2 (the column-panel SpMV over operators far larger than
+// L2, where the gathered vector slice must stay resident).
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+template <bool kEF>
+__device__ __forceinline__ int4 ld_stream_i4_t(const int* p) {
+  if (!kEF) return ld_stream_i4(p);
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(l2_evict_first_policy()));
+  return r;
+}
+template <bool kEF>
+__device__ __forceinline__ int ld_stream_i1_t(const int* p) {
+  if (!kEF) return ld_stream_i1(p);
+  int r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
+               : "=r"(r)
+               : "l"(p), "l"(l2_evict_first_policy()));
+  return r;
+}
+template <bool kEF>
+__device__ __forceinline__ double ld_stream_d1_t(const double* p) {
+  if (!kEF) return ld_stream_d1(p);
+  double r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+               : "=d"(r)
+               : "l"(p), "l"(l2_evict_first_policy()));
+  return r;
+}
+template <bool kEF>
+__device__ __forceinline__ double2 ld_stream_d2_t(const double* p) {
+  if (!kEF) return ld_stream_d2(p);
+  double2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+               : "=d"(r.x), "=d"(r.y)
+               : "l"(p), "l"(l2_evict_first_policy()));
   return r;
 }
 

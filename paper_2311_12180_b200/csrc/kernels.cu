@@ -1099,6 +1099,18 @@ __global__ void fill_int_kernel(int* p, int64_t n, int v) {
 }
 
 // One warp per row: max |v * (d_self[r] * d_other[col])| (order-free, exact).
+// Short rows: one thread per row (max is order-free, so any assignment gives
+// the same bits).
+__global__ void row_absmax_thread_kernel(const int* rp, const int* col, const double* val, int rows,
+                                         const double* d_self, const double* d_other, double* out) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+    const double dr = d_self[r];
+    double mx = 0.0;
+    for (int k = rp[r]; k < rp[r + 1]; ++k) mx = smax(mx, fabs(val[k] * (dr * d_other[col[k]])));
+    out[r] = mx;
+  }
+}
+
 __global__ void row_absmax_kernel(const int* rp, const int* col, const double* val, int rows,
                                   const double* d_self, const double* d_other, double* out) {
   const int lane = threadIdx.x & 31;
@@ -1274,9 +1286,13 @@ void launch_fill_int(int* p, int64_t n, int v, cudaStream_t s) {
   PDLP_CUDA(cudaGetLastError());
 }
 void launch_row_absmax(const int* rp, const int* col, const double* val, int rows,
-                       const double* d_self, const double* d_other, double* out, cudaStream_t s) {
-  row_absmax_kernel<<<grid_for(int64_t(rows) * 32), kThreads, 0, s>>>(rp, col, val, rows, d_self,
-                                                                     d_other, out);
+                       const double* d_self, const double* d_other, double* out, cudaStream_t s,
+                       double avg_len) {
+  if (avg_len <= 8.0)
+    row_absmax_thread_kernel<<<grid_for(rows), kThreads, 0, s>>>(rp, col, val, rows, d_self, d_other, out);
+  else
+    row_absmax_kernel<<<grid_for(int64_t(rows) * 32), kThreads, 0, s>>>(rp, col, val, rows, d_self,
+                                                                       d_other, out);
   PDLP_CUDA(cudaGetLastError());
 }
 void launch_row_pnorm(const int* rp, const int* col, const double* val, int rows,

@@ -35,7 +35,8 @@ void launch_row_contig(const int* rp, const int* col, int rows, int min_len, int
 void launch_fill_int(int* p, int64_t n, int v, cudaStream_t s);
 // Ruiz (scaling.hpp:52-66): out[r] = max_k |v_k * (d_row[r] * d_col[col_k])|
 void launch_row_absmax(const int* rp, const int* col, const double* val, int rows,
-                       const double* d_self, const double* d_other, double* out, cudaStream_t s);
+                       const double* d_self, const double* d_other, double* out, cudaStream_t s,
+                       double avg_len = 1e9);
 // Pock-Chambolle (scaling.hpp:72-94): out[r] = sequential sum_k |v*(d*d)|^p, then the
 // row's pow(acc, 1/p) exactly as row_norms/col_norms (sparse_matrix.hpp:212-255)
 void launch_row_pnorm(const int* rp, const int* col, const double* val, int rows,

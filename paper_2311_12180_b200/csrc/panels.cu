@@ -29,8 +29,9 @@ int grid_n(int64_t n) {
 
 struct PartialEpi : EpiBase<PartialEpi> {
   static constexpr int NP = 1, NA = 1, NR = 1;
-  static constexpr bool kUniform = true;
-  static constexpr TileGeom kGeom = kIterGeom;
+  static constexpr bool kEvictFirst = true;  // the stacked operator streams through L2 once per pass
+  // (no kUniform: stacked rows are short and irregular)
+  static constexpr TileGeom kGeom = kPanelGeom;
   static constexpr bool kNeedCol = false;
   const double* __restrict__ x;
   double* __restrict__ out;

@@ -115,6 +115,13 @@ Solver::Solver(const pdlp_lp& lp, const pdlp_params& params) : params_(params) {
   const auto t = std::chrono::steady_clock::now();
   validate_input(lp, params);
   PDLP_CUDA(cudaSetDevice(params.device));
+  {
+    // the stream-ordered pool keeps freed memory for the next handle
+    cudaMemPool_t pool;
+    PDLP_CUDA(cudaDeviceGetDefaultMemPool(&pool, params.device));
+    uint64_t keep = ~uint64_t(0);
+    PDLP_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  }
   PDLP_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   if (!std::getenv("PDLP_NO_EVAL_FORK")) {
     PDLP_CUDA(cudaStreamCreateWithFlags(&fork_.s2, cudaStreamNonBlocking));
@@ -127,6 +134,7 @@ Solver::Solver(const pdlp_lp& lp, const pdlp_params& params) : params_(params) {
 }
 
 Solver::~Solver() {
+  if (stream_) cudaStreamSynchronize(stream_);  // pool frees below are stream-ordered
   for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
   if (ev_begin_) cudaEventDestroy(ev_begin_);
   if (ev_end_) cudaEventDestroy(ev_end_);
@@ -397,7 +405,7 @@ void Solver::build_panels(PanelOp& po, OpPlan& plan, const DevCsr& op, int rows,
   PDLP_CUDA(cudaMemcpyAsync(rp_h.data(), po.rp.get(), rp_h.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
   PDLP_CUDA(cudaStreamSynchronize(s));
   const DevCsr base{po.rp.get(), po.col.get(), po.val.get(), nullptr, srows, cols, nnz};
-  build_plan(plan, base, rp_h, kIterGeom, {}, 0, srows);
+  build_plan(plan, base, rp_h, kPanelGeom, {}, 0, srows);
   po.partial.alloc(size_t(srows));
   po.panels = panels;
   po.width = width;
@@ -502,9 +510,9 @@ void Solver::precondition() {
   if (mode != PDLP_SCALING_NONE) {
     for (int it = 0; it < params_.ruiz_iterations; ++it) {  // ruiz_equilibrate :52-66
       launch_row_absmax(k_rp_.get(), k_col_.get(), k_val_orig_.get(), int(m_), d1_dev_.get(),
-                        d2_dev_.get(), rn.get(), s);
+                        d2_dev_.get(), rn.get(), s, double(nnz_) / double(std::max<int64_t>(1, m_)));
       launch_row_absmax(kt_rp_.get(), kt_col_.get(), kt_val_orig_.get(), int(n_), d2_dev_.get(),
-                        d1_dev_.get(), cn.get(), s);
+                        d1_dev_.get(), cn.get(), s, double(nnz_) / double(std::max<int64_t>(1, n_)));
       launch_ruiz_update(d1_dev_.get(), rn.get(), int(m_), s);
       launch_ruiz_update(d2_dev_.get(), cn.get(), int(n_), s);
     }
@@ -588,12 +596,13 @@ void Solver::pin_iterates_in_l2() {
 
 void Solver::allocate_iteration() {
   cudaStream_t s = stream_;
-  x_all_.alloc(3 * size_t(n_));
-  y_all_.alloc(3 * size_t(m_));
+  const bool ipc = world_ > 1;  // exchanged buffers must be CUDA-IPC capable
+  x_all_.alloc(3 * size_t(n_), ipc);
+  y_all_.alloc(3 * size_t(m_), ipc);
   for (auto& b : kx_) b.alloc(m_);
   for (auto& b : kty_) b.alloc(n_);
-  avg_x_.alloc(n_);
-  avg_y_.alloc(m_);
+  avg_x_.alloc(n_, ipc);
+  avg_y_.alloc(m_, ipc);
   x_start_.alloc(n_);
   y_start_.alloc(m_);
   const int64_t row0 = k_cuts_[rank_], row1 = k_cuts_[rank_ + 1];
@@ -604,8 +613,8 @@ void Solver::allocate_iteration() {
   // block when the operator runs as column panels
   const int k_tiles = kpan_.panels ? panel_combine_blocks(int(m_)) : int(k_it_.plan.tiles.size());
   const int kt_tiles = ktpan_.panels ? panel_combine_blocks(int(n_)) : int(kt_it_.plan.tiles.size());
-  d_part_.alloc(size_t(k_tiles) * 3);
-  p_part_.alloc(size_t(kt_tiles) * 4 + 2);  // two parity buffers + dx^2 total
+  d_part_.alloc(size_t(k_tiles) * 3, ipc);
+  p_part_.alloc(size_t(kt_tiles) * 4 + 2, ipc);  // two parity buffers + dx^2 total
   p_part_.zero(s);
   const bool seq = parity();
   seq_dy2_.alloc(seq ? m_ : 1);
@@ -707,14 +716,14 @@ void Solver::allocate_iteration() {
 
   X4_.alloc(size_t(n_) * 4);
   Y4_.alloc(size_t(m_) * 4);
-  lam_.alloc(size_t(n_) * 4);
+  lam_.alloc(size_t(n_) * 4, world_ > 1);
   scratch_n_.alloc(n_);
   scratch_m_.alloc(m_);
   const int grid0 = eval_grid0(int(n_), int(m_));
   part0_.alloc(size_t(std::max(1, grid0)) * 4);
   const int ev1_tiles = int(k_ev_.plan.tiles.size()), ev2_tiles = int(kt_ev_.plan.tiles.size());
-  part1_.alloc(size_t(ev1_tiles) * 14);
-  part2_.alloc(size_t(ev2_tiles) * 18);
+  part1_.alloc(size_t(ev1_tiles) * 14, world_ > 1);
+  part2_.alloc(size_t(ev2_tiles) * 18, world_ > 1);
   seq_r_.alloc(seq ? size_t(m_) * 4 : 1);
   seq_d_.alloc(seq ? size_t(n_) * 4 : 1);
 
@@ -742,7 +751,7 @@ void Solver::allocate_iteration() {
   ev.stage = eval_stage_.get();
 
   // sharding: own slices, sync block, peer table (own entries until linked)
-  sync_.alloc(1);
+  sync_.alloc(1, world_ > 1);
   sync_.zero(s);
   shv_dev_.alloc(1);
   it.world = world_, it.rank = rank_;

@@ -26,22 +26,34 @@ class DevBuf {
   explicit DevBuf(size_t n) { alloc(n); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+  DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_), ipc_(o.ipc_) { o.p_ = nullptr; o.n_ = 0; }
   DevBuf& operator=(DevBuf&& o) noexcept {
     if (this != &o) {
       release();
       p_ = o.p_;
       n_ = o.n_;
+      ipc_ = o.ipc_;
       o.p_ = nullptr;
       o.n_ = 0;
     }
     return *this;
   }
   ~DevBuf() { release(); }
-  void alloc(size_t n) {
+  // Device memory comes from the device's stream-ordered pool (kept across
+  // handles: creating and destroying a solver does not round-trip through the
+  // driver's allocator); `ipc` buffers (exported to peer processes) use
+  // cudaMalloc, which CUDA IPC requires.
+  void alloc(size_t n, bool ipc = false) {
     release();
     n_ = n;
-    PDLP_CUDA(cudaMalloc(&p_, (n ? n : 1) * sizeof(T)));
+    ipc_ = ipc;
+    const size_t bytes = (n ? n : 1) * sizeof(T);
+    if (ipc) {
+      PDLP_CUDA(cudaMalloc(&p_, bytes));
+    } else {
+      PDLP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), bytes, cudaStreamPerThread));
+      PDLP_CUDA(cudaStreamSynchronize(cudaStreamPerThread));
+    }
   }
   void zero(cudaStream_t s) { PDLP_CUDA(cudaMemsetAsync(p_, 0, (n_ ? n_ : 1) * sizeof(T), s)); }
   T* get() const { return p_; }
@@ -49,11 +61,17 @@ class DevBuf {
 
  private:
   void release() {
-    if (p_) cudaFree(p_);
+    if (p_) {
+      if (ipc_)
+        cudaFree(p_);
+      else
+        cudaFreeAsync(p_, cudaStreamPerThread);
+    }
     p_ = nullptr;
   }
   T* p_ = nullptr;
   size_t n_ = 0;
+  bool ipc_ = false;
 };
 
 template <class T>

@@ -14,6 +14,16 @@
 
 namespace pdlp {
 
+// Epilogues opt in to L2 evict-first matrix streams with
+// `static constexpr bool kEvictFirst` (column-panel passes only).
+template <class Epi, class = void>
+struct has_evict_first { static constexpr bool value = false; };
+template <class Epi>
+struct has_evict_first<Epi, decltype(void(Epi::kEvictFirst))> { static constexpr bool value = Epi::kEvictFirst; };
+template <class Epi>
+__host__ __device__ constexpr bool evict_first() { return has_evict_first<Epi>::value; }
+
+
 // Epi concept:
 //   static constexpr int NP, NA, NR; static constexpr bool kNeedCol;
 //   __device__ void gather(int col, double (&g)[NP]) const;
@@ -94,9 +104,9 @@ __device__ __forceinline__ void strided_partial(const Epi& epi, const int* __res
       const int q = q0 + u * nthreads;
       if (q < nq) {
         const int k = base + 4 * q;
-        const int4 c4 = ld_stream_i4(col + k);
-        const double2 va = ld_stream_d2(val + k);
-        const double2 vb = ld_stream_d2(val + k + 2);
+        const int4 c4 = ld_stream_i4_t<evict_first<Epi>()>(col + k);
+        const double2 va = ld_stream_d2_t<evict_first<Epi>()>(val + k);
+        const double2 vb = ld_stream_d2_t<evict_first<Epi>()>(val + k + 2);
         cs[u][0] = c4.x, cs[u][1] = c4.y, cs[u][2] = c4.z, cs[u][3] = c4.w;
         vs[u][0] = va.x, vs[u][1] = va.y, vs[u][2] = vb.x, vs[u][3] = vb.y;
       } else {
@@ -148,8 +158,8 @@ __device__ __forceinline__ void elem_partial(const Epi& epi, const int* __restri
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int e = e0 + u * nthreads;
-      cs[u] = e < k1 ? ld_stream_i1(col + e) : 0;
-      vs[u] = e < k1 ? ld_stream_d1(val + e) : 0.0;
+      cs[u] = e < k1 ? ld_stream_i1_t<evict_first<Epi>()>(col + e) : 0;
+      vs[u] = e < k1 ? ld_stream_d1_t<evict_first<Epi>()>(val + e) : 0.0;
     }
     double g[U][Epi::NP];
 #pragma unroll
@@ -213,8 +223,8 @@ __device__ __forceinline__ void uniform_rows(const Tile& t, const int* __restric
       const int k = t.k0 + (r - t.row0) * L;
 #pragma unroll
       for (int j = 0; j < L; ++j) {
-        cs[h][j] = r < t.row1 ? ld_stream_i1(col + k + j) : 0;
-        vs[h][j] = r < t.row1 ? ld_stream_d1(val + k + j) : 0.0;
+        cs[h][j] = r < t.row1 ? ld_stream_i1_t<evict_first<Epi>()>(col + k + j) : 0;
+        vs[h][j] = r < t.row1 ? ld_stream_d1_t<evict_first<Epi>()>(val + k + j) : 0.0;
       }
     }
 #pragma unroll
@@ -275,9 +285,9 @@ __device__ void run_tile(const Tile& t, const int* __restrict__ rp, const int* _
         const int q = q0 + u * kThreads;
         if (q < nq) {
           const int k = base + 4 * q;
-          const int4 c4 = ld_stream_i4(col + k);
-          const double2 va = ld_stream_d2(val + k);
-          const double2 vb = ld_stream_d2(val + k + 2);
+          const int4 c4 = ld_stream_i4_t<evict_first<Epi>()>(col + k);
+          const double2 va = ld_stream_d2_t<evict_first<Epi>()>(val + k);
+          const double2 vb = ld_stream_d2_t<evict_first<Epi>()>(val + k + 2);
           cs[u][0] = c4.x, cs[u][1] = c4.y, cs[u][2] = c4.z, cs[u][3] = c4.w;
           vs[u][0] = va.x, vs[u][1] = va.y, vs[u][2] = vb.x, vs[u][3] = vb.y;
         } else {
