@@ -715,6 +715,7 @@ struct Ev1Epi : EpiBase<Ev1Epi<kSeq>> {
 template <bool kSeq>
 struct Ev2Epi : EpiBase<Ev2Epi<kSeq>> {
   static constexpr int NP = 4, NA = 8, NR = 18;
+  static constexpr bool kUniform = true;  // K^T rows are often uniform (C1, C2, C4)
   static constexpr TileGeom kGeom = kEvalGeom;
   static constexpr bool kNeedCol = true;
   const double* __restrict__ Y4;

@@ -255,6 +255,40 @@ __device__ __forceinline__ void uniform_rows(const Tile& t, const int* __restric
   epi.template rows_strided<RPT>(t.row0 + tid, kThreads, nvalid, acc, red);
 }
 
+// Uniform short rows for wide epilogues (several points per gather, 4-8 sums
+// per row: the evaluation kernels): one row at a time, index order.
+template <class Epi, int L>
+__device__ __forceinline__ void uniform_rows_wide(const Tile& t, const int* __restrict__ col,
+                                                  const double* __restrict__ val, const Epi& epi,
+                                                  double (&red)[Epi::NR]) {
+  constexpr int RPT = Epi::kGeom.stream_rows / kThreads;
+#pragma unroll 1
+  for (int i = 0; i < RPT; ++i) {
+    const int r = t.row0 + threadIdx.x + i * kThreads;
+    if (r >= t.row1) break;
+    const int k = t.k0 + (r - t.row0) * L;
+    int cs[L];
+    double vs[L], g[L][Epi::NP];
+#pragma unroll
+    for (int j = 0; j < L; ++j) {
+      cs[j] = ld_stream_i1_t<evict_first<Epi>()>(col + k + j);
+      vs[j] = ld_stream_d1_t<evict_first<Epi>()>(val + k + j);
+    }
+#pragma unroll
+    for (int j = 0; j < L; ++j) epi.gather(cs[j], g[j]);
+    double acc[Epi::NA];
+    zero_acc<Epi>(acc);
+#pragma unroll
+    for (int j = 0; j < L; ++j) {
+      double p[Epi::NP];
+#pragma unroll
+      for (int q = 0; q < Epi::NP; ++q) p[q] = vs[j] * g[j][q];
+      epi.add(acc, p, cs[j]);
+    }
+    epi.row_done(r, acc, red);
+  }
+}
+
 // Processes one tile; `red` holds this thread's reduction terms.
 // `chunk_part` ([chunk_slots][NA]) and `chunk_ctr` ([split_rows]) serve split rows.
 template <class Epi, bool kSeq>
@@ -262,7 +296,17 @@ __device__ void run_tile(const Tile& t, const int* __restrict__ rp, const int* _
                          const double* __restrict__ val, const Epi& epi, double (&red)[Epi::NR],
                          double* chunk_part, unsigned* chunk_ctr, unsigned char* smem) {
   const int tid = threadIdx.x;
-  if (t.kind == kTileStream && t.part >= 1 && t.part <= 5 && Epi::NP == 1 && uniform_ok<Epi>()) {
+  if constexpr (Epi::NA > 2) {
+    if (t.kind == kTileStream && t.part >= 1 && t.part <= 4 && uniform_ok<Epi>()) {
+      switch (t.part) {
+        case 1: uniform_rows_wide<Epi, 1>(t, col, val, epi, red); return;
+        case 2: uniform_rows_wide<Epi, 2>(t, col, val, epi, red); return;
+        case 3: uniform_rows_wide<Epi, 3>(t, col, val, epi, red); return;
+        default: uniform_rows_wide<Epi, 4>(t, col, val, epi, red); return;
+      }
+    }
+  }
+  if (t.kind == kTileStream && t.part >= 1 && t.part <= 5 && Epi::NP == 1 && Epi::NA <= 2 && uniform_ok<Epi>()) {
     switch (t.part) {
       case 1: uniform_rows<Epi, 1>(t, col, val, epi, red); return;
       case 2: uniform_rows<Epi, 2>(t, col, val, epi, red); return;
