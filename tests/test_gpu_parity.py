@@ -388,3 +388,48 @@ def test_column_panels_match_oracle(which, monkeypatch):
     if r.status == SolveStatus.OPTIMAL:
         assert abs(r.info["primal_objective"] - o.info["primal_objective"]) <= 1e-5 * (
             1.0 + abs(o.info["primal_objective"]))
+
+
+# ---------------------------------------------------------------------------
+# fast mode over the whole reference suite (acceptance criteria 1/2/7 style)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", [n for n in suite_names()])
+def test_fast_mode_suite_status_objective_and_reference_check(name):
+    """Every suite instance (acceptance_main.cpp:79-154, 425-504) in fast mode:
+    same status as the reference; optimal points pass the reference's own
+    termination check at 1e-8 (criterion 2) and match its objective."""
+    lp = load_golden_lp(name)
+    ref = ref_suite()[name]
+    limit = 10000 if name.startswith("infeasible") else 1_000_000
+    r = solve(lp, SolverParams(eps_optimal=1e-8, iteration_limit=limit, time_limit_seconds=60.0))
+    assert str(r.status) == ref["status"]
+    if r.status == SolveStatus.OPTIMAL:
+        chk = O.check_termination(lp, r.point.primal, r.point.dual, 1e-8)
+        assert chk["terminated"]
+        assert abs(r.info["primal_objective"] - ref["primal_objective"]) <= 1e-6 * (
+            1.0 + abs(ref["primal_objective"]))
+
+
+@pytest.mark.parametrize("gen", ["multicommodity", "staircase"])
+def test_fast_mode_structured_generators_match_oracle(gen):
+    """The C3 / C5 generator shapes at small size: first 100 iterates within
+    1e-10 relative of the oracle, same status and objective at 1e-6."""
+    lp = {"multicommodity": lambda: generators.multicommodity_lp(300, 2000, 5, seed=4),
+          "staircase": lambda: generators.staircase_lp(3, 2000, 500, 500, seed=8)}[gen]()
+    ref = O.Session(lp, SolverParams(), "oracle")
+    with Solver(lp, SolverParams()) as s:
+        s.iterate_begin()
+        worst = 0.0
+        for k in range(100):
+            s.iterate_run(1)
+            ref.run(1)
+            a, b = s.iterate(), ref.iterate()
+            za, zb = np.concatenate([a["x"], a["y"]]), np.concatenate([b["x"], b["y"]])
+            worst = max(worst, float(np.linalg.norm(za - zb) / max(np.linalg.norm(zb), 1e-300)))
+    ref.close()
+    assert worst <= 1e-10
+    p = SolverParams(eps_optimal=1e-6, iteration_limit=200000)
+    r, o = solve(lp, p), O.solve(lp, p)
+    assert r.status == o.status == SolveStatus.OPTIMAL
+    assert abs(r.info["primal_objective"] - o.info["primal_objective"]) <= 1e-5 * (1.0 + abs(o.info["primal_objective"]))
