@@ -19,6 +19,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <utility>
 
 #include "../../include/pdlp_b200.h"
@@ -239,14 +240,14 @@ __global__ void __launch_bounds__(kThreads, 4) dual_kernel(DevCsr K, DevIter it,
   epi.m1 = it.m1;
   if (kShard) epi.push = PeerPush{it.shv->y_all, size_t(st->iy_trial) * it.m, it.world, it.rank};
   double red[3] = {0.0, 0.0, 0.0};
-  run_tile<DualEpi<kSeq, false, kShard>, kSeq>(t, K.rp, K.col, K.val, epi, red, K.chunk_part,
-                                               K.chunk_ctr, smem);
+  const int role = run_tile<DualEpi<kSeq, false, kShard>, kSeq>(t, K.rp, K.col, K.val, epi, red,
+                                                                K.chunk_part, K.chunk_ctr, smem);
   // the primal kernel's CTAs may start their prologue once every dual CTA is
   // past its tile (triggering earlier would let them take slots from our waves)
   griddep_launch_dependents();
-  store_partial<3, 0>(red, it.d_part, tile, it.d_tiles);
+  const PartialSlots ps = store_tile_partial<3, 0>(red, it.d_part, t, role, tile, it.d_tiles);
   if (kShard) {
-    push_partial<3>(it.shv->d_part, it.world, it.rank, 0, size_t(tile), size_t(it.d_tiles), red);
+    push_tile_partial<3, 0>(it.shv->d_part, it.world, it.rank, 0, ps, size_t(it.d_tiles), red);
     shard_signal(it.shv, it.sync, it.world, it.rank, kSyncDual);
     return;
   }
@@ -371,6 +372,7 @@ __global__ void __launch_bounds__(kThreads, 4) primal_kernel(DevCsr KT, DevIter 
   }
   if (d.mode == kPNone) return;  // keep the partials of the last real trial
   double red[2] = {0.0, 0.0};
+  int role = kRoleOwn;
   const double tau = d.eta / d.omega;  // tau = eta / omega, solver.hpp:401
   const PeerPush push{kShard ? it.shv->x_all : nullptr, size_t(d.ix_trial) * it.n, it.world, it.rank};
   if (bid >= KT.ntiles) {
@@ -424,8 +426,8 @@ __global__ void __launch_bounds__(kThreads, 4) primal_kernel(DevCsr KT, DevIter 
     epi.avg_first = d.first;
     epi.store_kty = (acc && !kSeq && it.kty_lazy) ? 0 : 1;
     epi.push = push;
-    run_tile<PrimalEpi<kSeq, kNonneg, false, kShard>, kSeq>(t, KT.rp, KT.col, KT.val, epi, red,
-                                                            KT.chunk_part, KT.chunk_ctr, smem);
+    role = run_tile<PrimalEpi<kSeq, kNonneg, false, kShard>, kSeq>(t, KT.rp, KT.col, KT.val, epi, red,
+                                                                   KT.chunk_part, KT.chunk_ctr, smem);
   } else if (d.mode == kPRetry) {
     // x' for the shrunk step over this tile's columns (a split column is
     // handled by its first slice), so the partials keep the tile layout
@@ -450,9 +452,9 @@ __global__ void __launch_bounds__(kThreads, 4) primal_kernel(DevCsr KT, DevIter 
   // ping-pong by trial parity: the next decision reads these while this launch's
   // late CTAs may still be reading the previous ones
   const size_t half = size_t(d.trials & 1) * it.p_tiles * 2;
-  store_partial<2, 0>(red, it.p_part + half, tile, it.p_tiles);
+  const PartialSlots ps = store_tile_partial<2, 0>(red, it.p_part + half, t, role, tile, it.p_tiles);
   if (kShard) {
-    push_partial<2>(it.shv->p_part, it.world, it.rank, half, size_t(tile), size_t(it.p_tiles), red);
+    push_tile_partial<2, 0>(it.shv->p_part, it.world, it.rank, half, ps, size_t(it.p_tiles), red);
     shard_signal(it.shv, it.sync, it.world, it.rank, kSyncPrimal);
   }
 }
@@ -788,11 +790,12 @@ __global__ void __launch_bounds__(kThreads, 3) eval_rows_kernel(DevCsr K, DevEva
   for (int i = 0; i < 14; ++i) red[i] = i < 12 ? 0.0 : -INFINITY;
   // one tile per CTA, one partial per (global) tile
   const int ti = K.tile0 + int(blockIdx.x);
-  run_tile<Ev1Epi<kSeq>, kSeq>(K.tiles[ti], K.rp, K.col, K.val_orig, epi, red, K.chunk_part,
-                               K.chunk_ctr, smem);
-  store_partial<12, 2>(red, ev.part1, ti, ev.ev1_tiles);
+  const Tile t = K.tiles[ti];
+  const int role = run_tile<Ev1Epi<kSeq>, kSeq>(t, K.rp, K.col, K.val_orig, epi, red, K.chunk_part,
+                                                K.chunk_ctr, smem);
+  const PartialSlots ps = store_tile_partial<12, 2>(red, ev.part1, t, role, ti, ev.ev1_tiles);
   if (ev.world > 1) {
-    push_partial<14>(ev.shv->part1, ev.world, ev.rank, 0, size_t(ti), size_t(ev.ev1_tiles), red);
+    push_tile_partial<12, 2>(ev.shv->part1, ev.world, ev.rank, 0, ps, size_t(ev.ev1_tiles), red);
     shard_signal(ev.shv, ev.sync, ev.world, ev.rank, kSyncEvRows);
   }
 }
@@ -809,11 +812,12 @@ __global__ void __launch_bounds__(kThreads) eval_cols_kernel(DevCsr KT, DevEval 
   for (int i = 0; i < 18; ++i) red[i] = i < 14 ? 0.0 : -INFINITY;
   epi.lam_push = PeerPush{ev.shv ? ev.shv->lam : nullptr, 0, ev.world, ev.rank};
   const int ti = KT.tile0 + int(blockIdx.x);
-  run_tile<Ev2Epi<kSeq>, kSeq>(KT.tiles[ti], KT.rp, KT.col, KT.val_orig, epi, red, KT.chunk_part,
-                               KT.chunk_ctr, smem);
-  store_partial<14, 4>(red, ev.part2, ti, ev.ev2_tiles);
+  const Tile t = KT.tiles[ti];
+  const int role = run_tile<Ev2Epi<kSeq>, kSeq>(t, KT.rp, KT.col, KT.val_orig, epi, red, KT.chunk_part,
+                                                KT.chunk_ctr, smem);
+  const PartialSlots ps = store_tile_partial<14, 4>(red, ev.part2, t, role, ti, ev.ev2_tiles);
   if (ev.world > 1) {
-    push_partial<18>(ev.shv->part2, ev.world, ev.rank, 0, size_t(ti), size_t(ev.ev2_tiles), red);
+    push_tile_partial<14, 4>(ev.shv->part2, ev.world, ev.rank, 0, ps, size_t(ev.ev2_tiles), red);
     shard_signal(ev.shv, ev.sync, ev.world, ev.rank, kSyncEvCols);
   }
 }
@@ -1355,8 +1359,9 @@ void launch_pdl(void (*kern)(P...), int grid, size_t smem, cudaStream_t s, A&&..
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  static const bool no_pdl = std::getenv("PDLP_NO_PDL") != nullptr;  // diagnostics
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = no_pdl ? 0 : 1;
   PDLP_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...));
 }
 }  // namespace

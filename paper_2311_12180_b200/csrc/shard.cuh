@@ -104,4 +104,19 @@ __device__ __forceinline__ void push_partial(double* const* field, int world, in
   for (int i = 0; i < W; ++i) push_peers(field, world, rank, base + size_t(i) * stride + slot, v[i]);
 }
 
+// push_partial for store_tile_partial's slots (the main slot gets `v`, the
+// identity slot zeros / -inf)
+template <int NS, int NM, class Slots>
+__device__ __forceinline__ void push_tile_partial(double* const* field, int world, int rank, size_t base,
+                                                  const Slots& ps, size_t stride,
+                                                  const double (&v)[NS + NM]) {
+  if (ps.main >= 0) push_partial<NS + NM>(field, world, rank, base, size_t(ps.main), stride, v);
+  if (ps.ident >= 0) {
+    double id[NS + NM];
+#pragma unroll
+    for (int i = 0; i < NS + NM; ++i) id[i] = i < NS ? 0.0 : -INFINITY;
+    push_partial<NS + NM>(field, world, rank, base, size_t(ps.ident), stride, id);
+  }
+}
+
 }  // namespace pdlp

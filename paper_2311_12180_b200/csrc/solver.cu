@@ -309,6 +309,18 @@ void Solver::setup(const pdlp_lp& lp) {
   build_plan(kt_win_, KT_, rpt_h, kWinGeom, {}, 0, n_);
   build_plan(k_ev_, K_, rp_h, kEvalGeom, kbrk, r0, r1, kc_p);
   build_plan(kt_ev_, KT_, rpt_h, kEvalGeom, ktbrk, c0, c1, ktc_p);
+  if (trace) {
+    for (const auto& pr : {std::make_pair("K", &k_it_), std::make_pair("KT", &kt_it_)}) {
+      const TilePlan& tp = pr.second->plan;
+      int uni = 0, shift = 0;
+      for (const Tile& t : tp.tiles) {
+        uni += (t.kind == kTileStream && t.part > 0) ? 1 : 0;
+        shift += (t.kind == kTileWarp && t.slot == 2) ? 1 : 0;
+      }
+      std::fprintf(stderr, "[pdlp setup] %s tiles: %d stream (%d uniform), %d warp (%d shifted), %d chunk\n",
+                   pr.first, tp.stream_tiles, uni, tp.warp_tiles, shift, tp.chunk_tiles);
+    }
+  }
   K_ = k_it_.csr;
   KT_ = kt_it_.csr;
   K_full_ = K_;

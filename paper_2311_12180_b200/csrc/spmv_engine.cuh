@@ -14,6 +14,9 @@
 
 namespace pdlp {
 
+// what run_tile did with the tile's reduction terms (see store_tile_partial)
+enum PartialRole : int { kRoleOwn = 0, kRoleSlice = 1, kRoleSliceLast = 2 };
+
 // Epilogues opt in to L2 evict-first matrix streams with
 // `static constexpr bool kEvictFirst` (column-panel passes only).
 template <class Epi, class = void>
@@ -291,28 +294,30 @@ __device__ __forceinline__ void uniform_rows_wide(const Tile& t, const int* __re
 
 // Processes one tile; `red` holds this thread's reduction terms.
 // `chunk_part` ([chunk_slots][NA]) and `chunk_ctr` ([split_rows]) serve split rows.
+// Returns the tile's partial role for store_tile_partial (kRoleOwn, or for a
+// slice of a split row kRoleSlice / kRoleSliceLast).
 template <class Epi, bool kSeq>
-__device__ void run_tile(const Tile& t, const int* __restrict__ rp, const int* __restrict__ col,
+__device__ int run_tile(const Tile& t, const int* __restrict__ rp, const int* __restrict__ col,
                          const double* __restrict__ val, const Epi& epi, double (&red)[Epi::NR],
                          double* chunk_part, unsigned* chunk_ctr, unsigned char* smem) {
   const int tid = threadIdx.x;
   if constexpr (Epi::NA > 2) {
     if (t.kind == kTileStream && t.part >= 1 && t.part <= 4 && uniform_ok<Epi>()) {
       switch (t.part) {
-        case 1: uniform_rows_wide<Epi, 1>(t, col, val, epi, red); return;
-        case 2: uniform_rows_wide<Epi, 2>(t, col, val, epi, red); return;
-        case 3: uniform_rows_wide<Epi, 3>(t, col, val, epi, red); return;
-        default: uniform_rows_wide<Epi, 4>(t, col, val, epi, red); return;
+        case 1: uniform_rows_wide<Epi, 1>(t, col, val, epi, red); return kRoleOwn;
+        case 2: uniform_rows_wide<Epi, 2>(t, col, val, epi, red); return kRoleOwn;
+        case 3: uniform_rows_wide<Epi, 3>(t, col, val, epi, red); return kRoleOwn;
+        default: uniform_rows_wide<Epi, 4>(t, col, val, epi, red); return kRoleOwn;
       }
     }
   }
   if (t.kind == kTileStream && t.part >= 1 && t.part <= 5 && Epi::NP == 1 && Epi::NA <= 2 && uniform_ok<Epi>()) {
     switch (t.part) {
-      case 1: uniform_rows<Epi, 1>(t, col, val, epi, red); return;
-      case 2: uniform_rows<Epi, 2>(t, col, val, epi, red); return;
-      case 3: uniform_rows<Epi, 3>(t, col, val, epi, red); return;
-      case 4: uniform_rows<Epi, 4>(t, col, val, epi, red); return;
-      default: uniform_rows<Epi, 5>(t, col, val, epi, red); return;
+      case 1: uniform_rows<Epi, 1>(t, col, val, epi, red); return kRoleOwn;
+      case 2: uniform_rows<Epi, 2>(t, col, val, epi, red); return kRoleOwn;
+      case 3: uniform_rows<Epi, 3>(t, col, val, epi, red); return kRoleOwn;
+      case 4: uniform_rows<Epi, 4>(t, col, val, epi, red); return kRoleOwn;
+      default: uniform_rows<Epi, 5>(t, col, val, epi, red); return kRoleOwn;
     }
   }
   if (t.kind == kTileStream) {
@@ -526,8 +531,10 @@ __device__ void run_tile(const Tile& t, const int* __restrict__ rp, const int* _
         chunk_ctr[t.row1] = 0u;
         epi.row_done(t.row0, tot, red);
       }
+      return last_part ? kRoleSliceLast : kRoleSlice;
     }
   }
+  return kRoleOwn;
 }
 
 // Block-reduces `red` in fixed order (NS sums then NM maxima) and writes it as
@@ -542,6 +549,34 @@ __device__ __forceinline__ void store_partial(double (&red)[NS + NM], double* pa
 #pragma unroll
     for (int i = 0; i < NS + NM; ++i) partials[size_t(i) * stride + slot] = red[i];
   }
+}
+
+// Where a tile's partial goes. A split row's reduction terms are added by
+// whichever of its slice CTAs arrives last, so they are stored under the row's
+// FIRST slice (and the other slices' partials hold the identity): the
+// fixed-order partial sums then do not depend on arrival order, and repeated
+// solves are bitwise identical.
+struct PartialSlots {
+  int main;   // slot receiving `red` (-1: none)
+  int ident;  // slot receiving the identity (-1: none)
+};
+__device__ __forceinline__ PartialSlots partial_slots(const Tile& t, int role, int tile) {
+  if (role == kRoleOwn) return {tile, -1};
+  const int first = tile - t.part;
+  if (role == kRoleSliceLast) return {first, t.part > 0 ? tile : -1};
+  return {-1, t.part > 0 ? tile : -1};  // the first slice's slot is the last CTA's
+}
+
+template <int NS, int NM>
+__device__ __forceinline__ PartialSlots store_tile_partial(double (&red)[NS + NM], double* partials,
+                                                          const Tile& t, int role, int tile, int stride) {
+  const PartialSlots ps = partial_slots(t, role, tile);
+  if (ps.main >= 0) store_partial<NS, NM>(red, partials, ps.main, stride);
+  if (ps.ident >= 0 && threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < NS + NM; ++i) partials[size_t(i) * stride + ps.ident] = i < NS ? 0.0 : -INFINITY;
+  }
+  return ps;
 }
 
 // Grid-level "am I the last CTA" ticket; resets the counter for the next replay.

@@ -215,6 +215,26 @@ def test_fast_mode_deterministic():
     assert np.array_equal(a.step_log, b.step_log)
 
 
+def test_split_rows_deterministic_across_runs():
+    """Split rows (CHUNK tiles) are finished by whichever slice CTA arrives
+    last; their reduction terms must still land in a fixed partial slot, or the
+    step sizes drift in the last bits from run to run (seen as ~20% of runs
+    differing before the fix)."""
+    lp = skewed_lp()
+    hashes, solves = set(), set()
+    for engine in (abi.ENGINE_GRAPH, abi.ENGINE_STREAM):
+        for _ in range(8):
+            with Solver(lp, SolverParams(eps_optimal=1e-6, iteration_limit=2, engine=engine)) as s:
+                s.iterate_begin()
+                s.iterate_run(2)
+                it = s.iterate()
+                hashes.add(sha(np.concatenate([it["x"], it["y"], it["kx"]])))
+        for _ in range(3):
+            r = solve(lp, SolverParams(eps_optimal=1e-6, engine=engine))
+            solves.add((r.iterations, sha(r.point.primal), sha(r.point.dual)))
+    assert len(hashes) == 1 and len(solves) == 1, (hashes, solves)
+
+
 def test_graph_and_stream_engines_bitwise():
     """Same per-trial kernels, replayed by a CUDA graph or launched one by one."""
     lp = generators.config("C1")
