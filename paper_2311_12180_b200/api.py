@@ -17,7 +17,8 @@ import numpy as np
 from . import abi
 from .lp import GeneralFormLp, SolveResult, SolverParams, result_from_buffers
 
-_LIB_PATH = Path(__file__).resolve().parent / "lib" / "libpdlp_b200.so"
+# PDLP_LIB selects an A/B build variant of the same library (tools/build_variants.py)
+_LIB_PATH = Path(os.environ.get("PDLP_LIB") or Path(__file__).resolve().parent / "lib" / "libpdlp_b200.so")
 _lib = None
 
 

@@ -14,6 +14,11 @@
 
 namespace pdlp {
 
+#ifndef PDLP_SHIFT_UNROLL
+#define PDLP_SHIFT_UNROLL 4
+#endif
+constexpr int kShiftUnroll = PDLP_SHIFT_UNROLL;  // elements in flight per lane in shifted-row groups
+
 // what run_tile did with the tile's reduction terms (see store_tile_partial)
 enum PartialRole : int { kRoleOwn = 0, kRoleSlice = 1, kRoleSliceLast = 2 };
 
@@ -84,8 +89,11 @@ struct EpiBase {
 };
 
 // Loads in flight per lane: 2 quads (8 nnz) per batch for the scalar-gather kernels.
+#ifndef PDLP_QUAD_UNROLL
+#define PDLP_QUAD_UNROLL 2
+#endif
 template <class Epi>
-__host__ __device__ constexpr int quad_unroll() { return Epi::NP == 1 ? 2 : 1; }
+__host__ __device__ constexpr int quad_unroll() { return Epi::NP == 1 ? PDLP_QUAD_UNROLL : 1; }
 
 // Strided partial sum over [k0, k1) by `nthreads` threads with lane index `t`,
 // using aligned 128-bit loads of indices and values; U quads of index/value
@@ -149,11 +157,10 @@ __device__ __forceinline__ void strided_partial(const Epi& epi, const int* __res
 // columns (one L1 wavefront per 32 gathers when a row's columns are
 // contiguous, instead of one per quad-strided lane). Used for WARP tiles whose
 // rows the planner found column-contiguous (Tile::slot == 1).
-template <class Epi>
+template <class Epi, int U = 4>
 __device__ __forceinline__ void elem_partial(const Epi& epi, const int* __restrict__ col,
                                              const double* __restrict__ val, int k0, int k1, int t,
                                              int nthreads, double (&acc)[Epi::NA]) {
-  constexpr int U = 4;
   zero_acc<Epi>(acc);
   for (int e0 = k0 + t; e0 < k1; e0 += nthreads * U) {
     int cs[U];
@@ -425,7 +432,7 @@ __device__ int run_tile(const Tile& t, const int* __restrict__ rp, const int* __
     const int r = t.row0 + (tid & 3);
     double acc[Epi::NA];
     zero_acc<Epi>(acc);
-    elem_partial(epi, col, val, rp[r], rp[r + 1], tid >> 2, kThreads / 4, acc);
+    elem_partial<Epi, kShiftUnroll>(epi, col, val, rp[r], rp[r + 1], tid >> 2, kThreads / 4, acc);
     __shared__ double sgrp4[kWarps * 4 * Epi::NA];
 #pragma unroll
     for (int i = 0; i < Epi::NA; ++i) {
