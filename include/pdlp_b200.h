@@ -235,6 +235,10 @@ enum {
 };
 
 int pdlp_abi_version(void);
+
+/* Number of visible CUDA devices (0 when the driver reports none); used by the
+ * benchmark harness to spread worker threads over GPUs (bench.hpp:212-222). */
+int pdlp_device_count(int32_t* count);
 void pdlp_default_params(pdlp_params* params);
 
 /* Validates (GeneralFormLp::validate lp_model.hpp:45-72, SolverParams::validate

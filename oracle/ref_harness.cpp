@@ -14,6 +14,10 @@
 //   spmv / spmv_transpose / explicit_transpose / from_triplets
 //                                       sparse_matrix.hpp:57-178
 //   read_mps_file                       mps_io.hpp:582-585
+//   config_hash / aggregate_records / write_report / run_benchmark
+//                                       bench.hpp:29-267
+//   restarted_pdhg_standard / kkt_error_standard / spectral_norm /
+//   p_s_norm_squared                    standard_form.hpp:36-211
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -24,7 +28,11 @@
 #include <string>
 #include <vector>
 
+#include <sstream>
+
+#include "pdhglp/bench.hpp"
 #include "pdhglp/mps_io.hpp"
+#include "pdhglp/standard_form.hpp"
 #include "pdhglp/scaling.hpp"
 #include "pdhglp/solver.hpp"
 #include "pdhglp/sparse_matrix.hpp"
@@ -565,5 +573,139 @@ void ref_mps_fill(void* hp, int64_t* g_off, int64_t* g_col, double* g_val, int64
 }
 
 void ref_mps_free(void* hp) { delete static_cast<MpsHold*>(hp); }
+
+// ---- benchmark harness (bench.hpp) ----
+int ref_bench_config_hash(const pdlp_params* p, double time_limit, char* out17) {
+  const std::string h = config_hash(to_params(*p), time_limit);
+  std::snprintf(out17, 17, "%s", h.c_str());
+  return 0;
+}
+
+int ref_bench_sgm(const double* t, int64_t n, double shift, double* out) {
+  try {
+    *out = shifted_geometric_mean(std::span<const double>(t, size_t(n)), shift);
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    return fail(PDLP_EINVAL, e.what());
+  }
+}
+
+static int copy_text(const std::string& s, char* buf, int64_t cap, int64_t* len) {
+  *len = int64_t(s.size());
+  if (buf && cap > 0) std::snprintf(buf, size_t(cap), "%s", s.c_str());
+  return int64_t(s.size()) < cap ? 0 : PDLP_EINVAL;
+}
+
+// write_report of records given column-wise (names '\n'-separated)
+int ref_bench_report(int64_t n, const char* names, const int64_t* nnz, const int32_t* parse_failed,
+                     const int32_t* status, const double* solve_s, const double* total_s, const int64_t* iters,
+                     const double* obj, const double* gap, const double* rpr, const double* rdr,
+                     const pdlp_params* p, double time_limit, char* buf, int64_t cap, int64_t* len) {
+  BenchmarkReport rep;
+  rep.config_line = config_hash(to_params(*p), time_limit);
+  rep.time_limit = time_limit;
+  std::istringstream ns(names);
+  for (int64_t i = 0; i < n; ++i) {
+    BenchmarkRecord r;
+    std::getline(ns, r.instance);
+    r.nonzeros = nnz[i];
+    r.parse_failed = parse_failed[i] != 0;
+    r.status = static_cast<SolveStatus>(status[i]);
+    r.solve_seconds = solve_s[i];
+    r.total_seconds = total_s[i];
+    r.iterations = iters[i];
+    r.primal_objective = obj[i];
+    r.relative_gap = gap[i];
+    r.relative_primal_residual = rpr[i];
+    r.relative_dual_residual = rdr[i];
+    rep.records.push_back(r);
+  }
+  rep.aggregates = aggregate_records(rep.records, time_limit);
+  std::ostringstream out;
+  write_report(rep, out);
+  return copy_text(out.str(), buf, cap, len);
+}
+
+int ref_bench_run(const char* dir, const pdlp_params* p, double time_limit, int32_t jobs, char* buf,
+                  int64_t cap, int64_t* len) {
+  try {
+    const BenchmarkReport rep = run_benchmark(dir, to_params(*p), time_limit, jobs);
+    std::ostringstream out;
+    write_report(rep, out);
+    return copy_text(out.str(), buf, cap, len);
+  } catch (const std::exception& e) {
+    return fail(PDLP_ERUNTIME, e.what());
+  }
+}
+
+// ---- standard-form theory harness (standard_form.hpp) ----
+static StandardFormLp to_standard(const pdlp_csr* a, const double* b, const double* c) {
+  StandardFormLp lp;
+  lp.constraint_matrix = to_csr(*a);
+  lp.rhs.assign(b, b + a->num_rows);
+  lp.objective.assign(c, c + a->num_cols);
+  return lp;
+}
+
+int ref_kkt_error_standard(const pdlp_csr* a, const double* b, const double* c, const double* x,
+                           const double* y, double* out) {
+  const StandardFormLp lp = to_standard(a, b, c);
+  *out = kkt_error_standard(lp, std::span<const double>(x, size_t(a->num_cols)),
+                            std::span<const double>(y, size_t(a->num_rows)));
+  return 0;
+}
+
+int ref_spectral_norm(const pdlp_csr* a, double tol, int32_t max_iterations, double* out) {
+  *out = spectral_norm(to_csr(*a), tol, max_iterations);
+  return 0;
+}
+
+int ref_p_s_norm_squared(const pdlp_csr* a, const double* b, const double* c, double s, const double* x,
+                         const double* y, double* out) {
+  const StandardFormLp lp = to_standard(a, b, c);
+  *out = p_s_norm_squared(lp, s, std::span<const double>(x, size_t(a->num_cols)),
+                          std::span<const double>(y, size_t(a->num_rows)));
+  return 0;
+}
+
+// restarted_pdhg_standard from z = 0 (or x0/y0 when given). Outputs: per epoch
+// start KKT and length (up to `cap` epochs), counters[4] = {epochs,
+// total_iterations, converged, numerical_failure}, and the last epoch's start
+// point (x_last, y_last).
+int ref_standard_pdhg(const pdlp_csr* a, const double* b, const double* c, double step, double decay,
+                      double tol, int64_t iteration_limit, const double* x0, const double* y0,
+                      double* start_kkt, int64_t* lengths, int64_t cap, int64_t* counters, double* x_last,
+                      double* y_last) {
+  try {
+    const StandardFormLp lp = to_standard(a, b, c);
+    StandardPdhgOptions o;
+    o.step_size = step;
+    o.restart_decay = decay;
+    o.convergence_tol = tol;
+    o.iteration_limit = iteration_limit;
+    PrimalDualPoint z0;
+    if (x0 && y0) {
+      z0.primal.assign(x0, x0 + a->num_cols);
+      z0.dual.assign(y0, y0 + a->num_rows);
+    }
+    const StandardPdhgTrace t = restarted_pdhg_standard(lp, o, z0);
+    const int64_t ne = int64_t(t.epochs.size());
+    for (int64_t e = 0; e < ne && e < cap; ++e) {
+      start_kkt[e] = t.epochs[size_t(e)].start_kkt;
+      lengths[e] = t.epochs[size_t(e)].length;
+    }
+    counters[0] = ne;
+    counters[1] = t.total_iterations;
+    counters[2] = t.converged ? 1 : 0;
+    counters[3] = t.numerical_failure ? 1 : 0;
+    if (ne > 0) {
+      copy_out(t.epochs.back().start.primal, x_last);
+      copy_out(t.epochs.back().start.dual, y_last);
+    }
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    return fail(PDLP_EINVAL, e.what());
+  }
+}
 
 }  // extern "C"

@@ -46,6 +46,7 @@ def load_library(build_if_missing: bool = True) -> C.CDLL:
     dp, i64p, i32p = C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_int32)
     sig = {
         "pdlp_abi_version": (C.c_int, []),
+        "pdlp_device_count": (C.c_int, [i32p]),
         "pdlp_default_params": (None, [C.POINTER(abi.PdlpParams)]),
         "pdlp_create": (C.c_int, [C.POINTER(abi.PdlpLp), C.POINTER(abi.PdlpParams), C.POINTER(H)]),
         "pdlp_destroy": (None, [H]),
@@ -340,6 +341,13 @@ def _lp_from_file(lib, h) -> GeneralFormLp:
     return GeneralFormLp(csr(v.inequality_matrix), csr(v.equality_matrix), vec(v.objective, n),
                          vec(v.inequality_rhs, m1), vec(v.equality_rhs, m2), vec(v.lower, n), vec(v.upper, n),
                          float(v.objective_constant))
+
+
+def device_count() -> int:
+    """Visible CUDA devices (pdlp_device_count)."""
+    n = C.c_int32(0)
+    _check(load_library().pdlp_device_count(C.byref(n)))
+    return int(n.value)
 
 
 def read_mps(path, fmt: int = MPS_AUTO) -> GeneralFormLp:

@@ -58,6 +58,17 @@ extern "C" {
 
 int pdlp_abi_version(void) { return PDLP_ABI_VERSION; }
 
+int pdlp_device_count(int32_t* count) {
+  if (!count) return PDLP_EINVAL;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  *count = n;
+  return PDLP_OK;
+}
+
 void pdlp_default_params(pdlp_params* p) {
   if (!p) return;
   std::memset(p, 0, sizeof *p);

@@ -60,3 +60,47 @@ def rel_err(a, b) -> float:
     if a.size == 0:
         return 0.0
     return float(np.max(np.abs(a - b)) / max(1.0, float(np.max(np.abs(b)))))
+
+
+def write_free_mps(lp: GeneralFormLp, path, name: str = "LP") -> None:
+    """Writes `lp` as free-format MPS that read_mps parses back to the same
+    GeneralFormLp (inequality rows as G rows first, then E rows; values with
+    17 significant digits; the objective constant as -RHS of the N row,
+    mps_io.hpp:403,508). Test helper: turns the golden .npz instances back
+    into files for the directory benchmark."""
+    G, A = lp.inequality_matrix, lp.equality_matrix
+    n, m1, m2 = lp.num_variables, G.num_rows, A.num_rows
+    f = lambda v: repr(float(v))  # noqa: E731  (shortest round-trip repr)
+    cols: list[list[tuple[str, float]]] = [[] for _ in range(n)]
+    for mat, prefix in ((G, "G"), (A, "E")):
+        for r in range(mat.num_rows):
+            for k in range(int(mat.row_offsets[r]), int(mat.row_offsets[r + 1])):
+                cols[int(mat.col_indices[k])].append((f"{prefix}{r}", float(mat.values[k])))
+    out = [f"NAME {name}", "ROWS", " N OBJ"]
+    out += [f" G G{r}" for r in range(m1)] + [f" E E{r}" for r in range(m2)]
+    out.append("COLUMNS")
+    for j in range(n):
+        out.append(f" X{j} OBJ {f(lp.objective[j])}")
+        out += [f" X{j} {row} {f(v)}" for row, v in cols[j]]
+    out.append("RHS")
+    if lp.objective_constant != 0.0:
+        out.append(f" RHS OBJ {f(-lp.objective_constant)}")
+    out += [f" RHS G{r} {f(v)}" for r, v in enumerate(lp.inequality_rhs) if v != 0.0]
+    out += [f" RHS E{r} {f(v)}" for r, v in enumerate(lp.equality_rhs) if v != 0.0]
+    out.append("BOUNDS")
+    inf = float("inf")
+    for j, (lo, up) in enumerate(zip(lp.lower, lp.upper)):
+        if lo == up:
+            out.append(f" FX BND X{j} {f(lo)}")
+            continue
+        if lo == -inf and up == inf:
+            out.append(f" FR BND X{j}")
+            continue
+        if lo == -inf:
+            out.append(f" MI BND X{j}")
+        elif lo != 0.0:
+            out.append(f" LO BND X{j} {f(lo)}")
+        if up != inf:
+            out.append(f" UP BND X{j} {f(up)}")
+    out.append("ENDATA")
+    Path(path).write_text("\n".join(out) + "\n")
