@@ -287,6 +287,51 @@ int pdlp_time_kernel(pdlp_handle* h, int32_t which, int32_t reps, double* avg_ms
 /* Problem sizes after create: {n, m, m1, nnz}. */
 int pdlp_get_sizes(pdlp_handle* h, int64_t* sizes);
 
+/* ---- standard-form theory harness (standard_form.hpp:36-211) ------------- */
+
+/* min c'x s.t. Ax = b, x >= 0 with A an m x n CSR (pdlp_csr), b (m), c (n).
+ * parity = 1: sequential sums in the reference's order (bitwise with
+ * restarted_pdhg_standard / kkt_error_standard / spectral_norm); 0: tiled,
+ * tree-reduced (fast). */
+typedef struct {
+  double step_size;        /* s, both primal and dual step; must be > 0 */
+  double restart_decay;    /* beta in (0, 1); default 0.5 */
+  double convergence_tol;  /* stop once the epoch-start KKT error <= this; default 1e-9 */
+  int64_t iteration_limit; /* default 1000000 */
+  int32_t parity;
+  int32_t device;
+  int64_t reserved[4];
+} pdlp_standard_options;
+
+void pdlp_standard_default_options(pdlp_standard_options* options);
+
+/* restarted_pdhg_standard (standard_form.hpp:131-211) on the GPU, from z = 0
+ * or (x0, y0) when both are given. Per epoch (up to `cap`): its start KKT
+ * error and length. counters[4] = {epochs, total_iterations, converged,
+ * numerical_failure}. x_out (n) / y_out (m), optional: the last epoch's
+ * start point. iter_x ([iter_cap][n]) /
+ * iter_y ([iter_cap][m]), optional: record_iterates, the iterate after each of
+ * the first iter_cap iterations (epoch by epoch, split by `lengths`). Invalid
+ * options return PDLP_EINVAL with StandardPdhgOptions::validate's message. */
+int pdlp_standard_pdhg(const pdlp_csr* a, const double* b, const double* c, const pdlp_standard_options* options,
+                       const double* x0, const double* y0, double* start_kkt, int64_t* lengths, int64_t cap,
+                       int64_t* counters, double* x_out, double* y_out, double* iter_x, double* iter_y,
+                       int64_t iter_cap);
+
+/* kkt_error_standard (standard_form.hpp:37-58):
+ * ||(Ax - b; [-x]+; [A'y - c]+; [c'x - b'y]+)||_2 */
+int pdlp_kkt_error_standard(const pdlp_csr* a, const double* b, const double* c, const double* x,
+                            const double* y, int32_t parity, int32_t device, double* out);
+
+/* spectral_norm (standard_form.hpp:63-89): largest singular value of A by
+ * power iteration on A'A from the normalised all-ones vector. */
+int pdlp_spectral_norm(const pdlp_csr* a, double tol, int32_t max_iterations, int32_t parity, int32_t device,
+                       double* out);
+
+/* p_s_norm_squared (standard_form.hpp:92-98): ||x||^2 + ||y||^2 + 2 s y'Ax. */
+int pdlp_p_s_norm_squared(const pdlp_csr* a, const double* b, const double* c, double step, const double* x,
+                          const double* y, int32_t parity, int32_t device, double* out);
+
 /* ---- CSR construction on the GPU --------------------------------------- */
 
 /* CsrMatrix::from_triplets (sparse_matrix.hpp:57-108) on device `device`:

@@ -670,12 +670,12 @@ int ref_p_s_norm_squared(const pdlp_csr* a, const double* b, const double* c, do
 
 // restarted_pdhg_standard from z = 0 (or x0/y0 when given). Outputs: per epoch
 // start KKT and length (up to `cap` epochs), counters[4] = {epochs,
-// total_iterations, converged, numerical_failure}, and the last epoch's start
-// point (x_last, y_last).
+// total_iterations, converged, numerical_failure}, the last epoch's start
+// point (x_last, y_last), and with iter_x/iter_y the recorded iterates.
 int ref_standard_pdhg(const pdlp_csr* a, const double* b, const double* c, double step, double decay,
                       double tol, int64_t iteration_limit, const double* x0, const double* y0,
                       double* start_kkt, int64_t* lengths, int64_t cap, int64_t* counters, double* x_last,
-                      double* y_last) {
+                      double* y_last, double* iter_x, double* iter_y, int64_t iter_cap) {
   try {
     const StandardFormLp lp = to_standard(a, b, c);
     StandardPdhgOptions o;
@@ -683,6 +683,7 @@ int ref_standard_pdhg(const pdlp_csr* a, const double* b, const double* c, doubl
     o.restart_decay = decay;
     o.convergence_tol = tol;
     o.iteration_limit = iteration_limit;
+    o.record_iterates = iter_x && iter_y && iter_cap > 0;
     PrimalDualPoint z0;
     if (x0 && y0) {
       z0.primal.assign(x0, x0 + a->num_cols);
@@ -702,6 +703,14 @@ int ref_standard_pdhg(const pdlp_csr* a, const double* b, const double* c, doubl
       copy_out(t.epochs.back().start.primal, x_last);
       copy_out(t.epochs.back().start.dual, y_last);
     }
+    int64_t k = 0;
+    for (const StandardEpoch& e : t.epochs)
+      for (const PrimalDualPoint& z : e.iterates) {
+        if (k >= iter_cap) break;
+        std::copy(z.primal.begin(), z.primal.end(), iter_x + k * a->num_cols);
+        std::copy(z.dual.begin(), z.dual.end(), iter_y + k * a->num_rows);
+        ++k;
+      }
     return 0;
   } catch (const std::invalid_argument& e) {
     return fail(PDLP_EINVAL, e.what());

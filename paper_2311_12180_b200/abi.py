@@ -44,6 +44,20 @@ class PdlpCsr(C.Structure):
     ]
 
 
+class PdlpStandardOptions(C.Structure):
+    """pdlp_standard_options (StandardPdhgOptions, standard_form.hpp:100-113)."""
+
+    _fields_ = [
+        ("step_size", C.c_double),
+        ("restart_decay", C.c_double),
+        ("convergence_tol", C.c_double),
+        ("iteration_limit", C.c_int64),
+        ("parity", C.c_int32),
+        ("device", C.c_int32),
+        ("reserved", C.c_int64 * 4),
+    ]
+
+
 class PdlpLp(C.Structure):
     _fields_ = [
         ("inequality_matrix", PdlpCsr),

@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 #include <utility>
 
 #include "../../include/pdlp_b200.h"
@@ -1223,9 +1224,16 @@ int grid_for(int64_t n, int per = kThreads) {
 }  // namespace
 
 void set_kernel_attributes() {
-  static bool done = false;
-  if (done) return;
-  done = true;
+  // once per device (function attributes are per device), from any thread
+  static std::mutex mu;
+  static unsigned long long done = 0;
+  int dev = 0;
+  PDLP_CUDA(cudaGetDevice(&dev));
+  {
+    std::lock_guard<std::mutex> g(mu);
+    if (dev < 64 && (done >> dev) & 1ull) return;
+    if (dev < 64) done |= 1ull << dev;
+  }
   auto big = [](const void* f, size_t bytes) {
     PDLP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
   };
