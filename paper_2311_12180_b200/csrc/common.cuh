@@ -41,7 +41,10 @@ struct TileGeom {
   int lane_nnz;    // target nnz per lane in WARP tiles
   int chunk_nnz;   // nnz per CHUNK tile of a split row
 };
-constexpr TileGeom kIterGeom{4096, 1024, 16, 4096};
+#ifndef PDLP_ITER_ROWS
+#define PDLP_ITER_ROWS 1024
+#endif
+constexpr TileGeom kIterGeom{4096, PDLP_ITER_ROWS, 16, 4096};
 constexpr TileGeom kWinGeom{2048, 1024, 8, 2048};
 constexpr TileGeom kEvalGeom{1024, 1024, 8, 2048};
 // column-panel passes: stacked rows hold ~nnz/row/panels entries, so tiles take

@@ -19,7 +19,7 @@ import json, os, sys
 sys.path.insert(0, os.environ["ROOT"])
 from paper_2311_12180_b200 import Solver, SolverParams, generators
 lp = generators.config(os.environ["CFG"])
-s = Solver(lp, SolverParams())
+s = Solver(lp, SolverParams(engine=int(os.environ.get("AB_ENGINE", "0"))))
 r = s.solve(); r = s.solve()
 out = {"iters": r.iterations, "solve_ms": r.info["device_seconds"] * 1e3}
 for which, name in ((2, "K"), (3, "KT"), (0, "dual"), (1, "primal")):
