@@ -102,7 +102,9 @@ def main() -> None:
         (prof / f"{tag}_ncu.json").write_text(json.dumps(caps, indent=1))
         summary_path = prof / "ncu_summary.json"
         summary = json.loads(summary_path.read_text()) if summary_path.exists() else {}
-        for name, lst in caps.items():
+        # the cold-cache capture (caches flushed before each kernel) wins when
+        # present: roofline.traffic is the conservative DRAM figure
+        for name, lst in sorted(caps.items(), key=lambda kv: kv[0] == "cold"):
             by_kernel: dict = {}
             for d in lst:
                 if "dram_bytes_per_launch" in d:
