@@ -140,6 +140,7 @@ struct DevIter {
   DevState* snap;    // state the current trial's dual kernel ran on (fast mode)
   int d_tiles;       // global K tiles (dual partials the decision sums)
   int kty_lazy;      // 1: accepted steps do not store K'y' (recomputed by a retry)
+  int prefetch;      // 1: kernels pull their tile (and the primal its operands) to L2 early
   int decide_sep;    // 1: the step decision runs in its own one-CTA kernel (many
                      //    tiles); 0: every primal CTA recomputes it at its head
   double* seq_dy2;   // parity-mode per-row terms (m)

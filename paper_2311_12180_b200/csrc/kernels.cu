@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 4) dual_kernel(DevCsr K, DevIter it,
   const bool helper = !kSeq && blockIdx.x == 0;
   const int tile = K.tile0 + int(blockIdx.x) - (kSeq ? 0 : 1);  // global tile index
   const Tile t = K.tiles[helper ? K.tile0 : tile];
-  if (!helper) prefetch_tile(t, K.rp, K.col, K.val);
+  if (!helper && it.prefetch) prefetch_tile(t, K.rp, K.col, K.val);
   griddep_wait();  // x' and the state come from the previous primal kernel
   DevState* st = it.st;
   // A failed or completed window parks the remaining (stream-engine) launches;
@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, 4) primal_kernel(DevCsr KT, DevIter 
   __shared__ Decision sd;
   const int bid = blockIdx.x;
   const int tile = KT.tile0 + bid;  // global tile index (CTAs >= ntiles: avg_y slices)
-  if (bid < KT.ntiles) {
+  if (bid < KT.ntiles && it.prefetch) {
     const Tile tp = KT.tiles[tile];
     prefetch_tile(tp, KT.rp, KT.col, KT.val);
   }
@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(kThreads, 4) primal_kernel(DevCsr KT, DevIter 
   const bool lazy_retry = !kSeq && it.kty_lazy && d.mode == kPRetry && mode_override < 0;
   if (d.mode == kPAccept || d.mode == kPRestart || lazy_retry) {
     const bool acc = d.mode == kPAccept;
-    {
+    if (it.prefetch) {
       // the epilogue's contiguous operands of this tile's columns -> L2 while
       // the matrix and the gathers are in flight
       const int j0 = t.row0;

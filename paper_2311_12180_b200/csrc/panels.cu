@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(kThreads, 4) panel_spmv_kernel(DevCsr A, DevIt
                                                                  int mode_override) {
   extern __shared__ __align__(16) unsigned char smem[];
   const Tile t = A.tiles[blockIdx.x];
-  prefetch_tile(t, A.rp, A.col, A.val);
+  if (it.prefetch) prefetch_tile(t, A.rp, A.col, A.val);
   griddep_wait();
   const DevState* st = it.st;
   const double* src;

@@ -720,6 +720,13 @@ void Solver::allocate_iteration() {
   // fast per-trial kernels skip storing K'y' on accepted steps (8n bytes per
   // iteration); the persistent window kernel keeps its own cache
   it.kty_lazy = (!parity() && engine_ != PDLP_ENGINE_PERSISTENT && !std::getenv("PDLP_NO_LAZY_KTY")) ? 1 : 0;
+  // L2 prefetch of the tiles before griddepcontrol.wait (overlapping the
+  // previous kernel's tail) pays where the operators are mid-sized and mostly
+  // L2-resident: C2 123.9 -> 119.3 ms per solve. Tiny operators only pay the
+  // extra prologue (C1 20.2 -> 20.9 ms) and ones far beyond L2 lose the
+  // gathered vector to the prefetched lines (C3 200.5 -> 207.4 ms).
+  it.prefetch = (nnz_ >= (int64_t(1) << 20) && nnz_ <= (int64_t(8) << 20)) ? 1 : 0;
+  if (const char* e = std::getenv("PDLP_PREFETCH")) it.prefetch = std::atoi(e) != 0;
   if (engine_ == PDLP_ENGINE_PERSISTENT && parity())
     invalid("params: the persistent engine runs fast mode only");
   if (engine_ == PDLP_ENGINE_PERSISTENT) {
