@@ -738,6 +738,20 @@ void Solver::allocate_iteration() {
     wb_.wd_part = wd_part_.get();
     wb_.wp_part = wp_part_.get();
     wb_.bar = bar_.get();
+    auto split_list = [&](const OpPlan& p, DevBuf<int>& buf, const int*& ptr, int& count) {
+      std::vector<int> idx;
+      for (size_t i = 0; i < p.plan.tiles.size(); ++i) {
+        const Tile& t = p.plan.tiles[i];
+        if (t.kind == kTileChunk && t.nparts > 1 && t.part == 0) idx.push_back(int(i));
+      }
+      buf.alloc(std::max<size_t>(1, idx.size()));
+      if (!idx.empty())
+        PDLP_CUDA(cudaMemcpyAsync(buf.get(), idx.data(), idx.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+      ptr = buf.get();
+      count = int(idx.size());
+    };
+    split_list(k_win_, k_split_, wb_.k_split, wb_.k_nsplit);
+    split_list(kt_win_, kt_split_, wb_.kt_split, wb_.kt_nsplit);
   }
   it.st = state_dev_;
 
@@ -987,6 +1001,7 @@ void Solver::run_window(int target) {
     wb.p_src = p_from_window_ ? wb_.wp_part
                               : it_.p_part + size_t(st.trials_total & 1) * it_.p_tiles * 2;
     wb.p_src_count = p_from_window_ ? win_grid_ : it_.p_tiles;
+    wb.p_src_window = p_from_window_ ? 1 : 0;
     launch_window(k_win_.csr, kt_win_.csr, it_, wb, win_grid_, stream_);
     p_from_window_ = true;
     launches_ += 1;

@@ -270,6 +270,7 @@ class Solver {
   bool p_from_window_ = false;
   bool eval_fresh_ = false;  // EvalOut on the host matches the device state
   DevBuf<double> wd_part_, wp_part_;
+  DevBuf<int> k_split_, kt_split_;  // split rows of the window plans (first-slice tiles)
   DevBuf<GridBar> bar_;
   WinBufs wb_{};
   std::vector<pdlp_step_log_entry> step_log_;

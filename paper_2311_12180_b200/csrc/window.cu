@@ -204,9 +204,26 @@ __device__ __forceinline__ void staged_tile(const Tile& t, const Stage& sg, doub
         double tot[1] = {0.0};
         for (int p = 0; p < t.nparts; ++p) tot[0] += __ldcg(chunk_part + size_t(t.slot + p) * 8);
         chunk_ctr[t.row1] = 0u;
-        epi.row_done(t.row0, tot, red);
+        // the row's reduction terms go to a fixed place (the first slice's
+        // chunk slot), not into this CTA's partial: see WinBufs::k_split
+        double rr[Epi::NR];
+#pragma unroll
+        for (int i = 0; i < Epi::NR; ++i) rr[i] = 0.0;
+        epi.row_done(t.row0, tot, rr);
+#pragma unroll
+        for (int i = 0; i < Epi::NR; ++i) chunk_part[size_t(t.slot) * 8 + 1 + i] = rr[i];
       }
     }
+  }
+}
+
+// adds the split rows' terms (fixed order) to the leader's sums
+template <int NR>
+__device__ __forceinline__ void add_split_terms(const DevCsr& op, const int* split, int nsplit, double (&sum)[NR]) {
+  for (int s = 0; s < nsplit; ++s) {
+    const Tile& t = op.tiles[split[s]];
+#pragma unroll
+    for (int i = 0; i < NR; ++i) sum[i] += __ldcg(op.chunk_part + size_t(t.slot) * 8 + 1 + i);
   }
 }
 
@@ -316,6 +333,7 @@ __global__ void __launch_bounds__(kThreads, 2) window_kernel(DevCsr K, DevCsr KT
   // the primal partials of the trial x' produced before this launch
   const double* p_src = wb.p_src;
   int p_count = wb.p_src_count;
+  int p_window = wb.p_src_window;
 
   for (;;) {
     // ================= D phase (dual update of this trial) =================
@@ -347,6 +365,8 @@ __global__ void __launch_bounds__(kThreads, 2) window_kernel(DevCsr K, DevCsr KT
       sum_partials<3, 0>(wb.wd_part, nctas, dp);
       sum_partials<2, 0>(p_src, p_count, pp);
       if (threadIdx.x != 0) return;
+      add_split_terms<3>(K, wb.k_split, wb.k_nsplit, dp);
+      if (p_window) add_split_terms<2>(KT, wb.kt_split, wb.kt_nsplit, pp);
       const double dy2 = dp[0], inter = dp[1], dx2 = pp[0];
       const bool finite = dp[2] == 0.0 && pp[1] == 0.0;
       int cont = 0;
@@ -478,6 +498,7 @@ __global__ void __launch_bounds__(kThreads, 2) window_kernel(DevCsr K, DevCsr KT
     store_partial<2, 0>(pred, wb.wp_part, cta, nctas);
     p_src = wb.wp_part;
     p_count = nctas;
+    p_window = mode == kPRetry ? 0 : 1;  // a retry phase ran no split columns
     if (!cont) break;
     grid_barrier(wb.bar, unsigned(nctas), []() {});
   }

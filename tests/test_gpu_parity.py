@@ -233,6 +233,11 @@ def test_split_rows_deterministic_across_runs():
             r = solve(lp, SolverParams(eps_optimal=1e-6, engine=engine))
             solves.add((r.iterations, sha(r.point.primal), sha(r.point.dual)))
     assert len(hashes) == 1 and len(solves) == 1, (hashes, solves)
+    # the persistent window kernel keeps per-CTA partials: its split-row terms
+    # go to fixed chunk slots that the barrier leader adds in order
+    pers = {(r.iterations, sha(r.point.primal), sha(r.point.dual))
+            for r in (solve(lp, SolverParams(eps_optimal=1e-6, engine=abi.ENGINE_PERSISTENT)) for _ in range(4))}
+    assert len(pers) == 1, pers
 
 
 def test_graph_and_stream_engines_bitwise():
