@@ -47,10 +47,30 @@ def env_rank():
 
 
 def peaks():
+    """HBM peak for the roofline: MEASURED_PEAKS.json (driver-written) when
+    present -- its burst figure, since the dominant kernel is timed alone --
+    else the 6650 GB/s fallback of B200_PROFILING.md."""
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
-        d = json.loads(p.read_text())
-        return float(d.get("hbm_gbs", 6650.0)), "measured"
+        try:
+            d = json.loads(p.read_text())
+        except ValueError:
+            d = {}
+        flat = {}
+
+        def walk(o, pre=""):
+            if isinstance(o, dict):
+                for k, v in o.items():
+                    walk(v, f"{pre}{k}.".lower())
+            elif isinstance(o, (int, float)) and not isinstance(o, bool):
+                flat[pre.rstrip(".")] = float(o)
+
+        walk(d)
+        hbm = {k: v for k, v in flat.items() if "hbm" in k and v > 100.0}
+        for pref in ("burst", "hbm_gbs", "copy", "sustained", ""):
+            cand = [v for k, v in sorted(hbm.items()) if pref in k]
+            if cand:
+                return cand[0], "measured"
     return 6650.0, "fallback"
 
 
