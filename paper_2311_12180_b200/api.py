@@ -148,9 +148,9 @@ class Solver:
     def result(self) -> SolveResult:
         info = self.last_info
         n, m = self.n, self.m
-        x, y = np.zeros(n), np.zeros(m)
-        lam, pos, neg = np.zeros(n), np.zeros(n), np.zeros(n)
-        _check(self._lib.pdlp_get_solution(self._h, *(abi.dptr(a) for a in (x, y, lam, pos, neg))))
+        x, y, lam = np.empty(n), np.empty(m), np.empty(n)
+        _check(self._lib.pdlp_get_solution(self._h, abi.dptr(x), abi.dptr(y), abi.dptr(lam), None, None))
+        pos = neg = None  # formed from lambda on first use (ReducedCosts)
         slog = np.zeros(info.step_log_size, abi.STEP_LOG_DTYPE)
         rlog = np.zeros(info.restart_log_size, abi.RESTART_DTYPE)
         if slog.size:

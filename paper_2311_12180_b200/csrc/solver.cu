@@ -13,6 +13,8 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <mutex>
+#include <map>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -305,8 +307,10 @@ void Solver::setup(const pdlp_lp& lp) {
   }
   build_plan(k_it_, K_, rp_h, kIterGeom, kbrk, r0, r1, kc_p);
   build_plan(kt_it_, KT_, rpt_h, kIterGeom, ktbrk, c0, c1, ktc_p);
-  build_plan(k_win_, K_, rp_h, kWinGeom, {}, 0, m_);
-  build_plan(kt_win_, KT_, rpt_h, kWinGeom, {}, 0, n_);
+  if (params_.engine == PDLP_ENGINE_PERSISTENT) {  // only the window kernel uses these
+    build_plan(k_win_, K_, rp_h, kWinGeom, {}, 0, m_);
+    build_plan(kt_win_, KT_, rpt_h, kWinGeom, {}, 0, n_);
+  }
   build_plan(k_ev_, K_, rp_h, kEvalGeom, kbrk, r0, r1, kc_p);
   build_plan(kt_ev_, KT_, rpt_h, kEvalGeom, ktbrk, c0, c1, ktc_p);
   if (trace) {
@@ -1162,6 +1166,41 @@ void Solver::evaluation_block() {
   restart_log_.push_back(ev);
   kkt_epoch_start_ = rc.weighted(st.omega);
   kkt_last_ = kkt_epoch_start_;
+}
+
+namespace {
+std::mutex& pinned_pool_mu() {
+  static std::mutex mu;
+  return mu;
+}
+// blocks are kept for the life of the process (bounded by peak concurrent use)
+std::multimap<size_t, void*>& pinned_pool() {
+  static auto* pool = new std::multimap<size_t, void*>();
+  return *pool;
+}
+}  // namespace
+
+void* pinned_pool_get(size_t bytes, size_t* capacity) {
+  std::lock_guard<std::mutex> g(pinned_pool_mu());
+  auto& pool = pinned_pool();
+  // smallest free block that fits, if it is not wastefully large
+  auto it = pool.lower_bound(bytes);
+  if (it != pool.end() && it->first <= 2 * bytes + (size_t(1) << 20)) {
+    void* p = it->second;
+    *capacity = it->first;
+    pool.erase(it);
+    return p;
+  }
+  void* p = nullptr;
+  const size_t cap = std::max<size_t>(bytes, 64);
+  PDLP_CUDA(cudaMallocHost(&p, cap));
+  *capacity = cap;
+  return p;
+}
+
+void pinned_pool_put(void* p, size_t capacity) {
+  std::lock_guard<std::mutex> g(pinned_pool_mu());
+  pinned_pool().emplace(capacity, p);
 }
 
 void Solver::finish_candidate(int status, const std::string& msg) {

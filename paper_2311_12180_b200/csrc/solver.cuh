@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <condition_variable>
 #include <memory>
@@ -72,6 +73,40 @@ class DevBuf {
   T* p_ = nullptr;
   size_t n_ = 0;
   bool ipc_ = false;
+};
+
+// Page-locked host memory from a process-wide pool: cudaMallocHost costs
+// milliseconds per call, so result buffers are recycled across solver handles.
+void* pinned_pool_get(size_t bytes, size_t* capacity);
+void pinned_pool_put(void* p, size_t capacity);
+
+// A resizable page-locked double array (the solve's result vectors: the D2H of
+// x, y and lambda at full PCIe rate instead of the pageable staging path).
+class PinnedVec {
+ public:
+  PinnedVec() = default;
+  PinnedVec(const PinnedVec&) = delete;
+  PinnedVec& operator=(const PinnedVec&) = delete;
+  ~PinnedVec() {
+    if (p_) pinned_pool_put(p_, cap_);
+  }
+  void assign(size_t n, double v) {
+    if (n * sizeof(double) > cap_) {
+      if (p_) pinned_pool_put(p_, cap_);
+      p_ = static_cast<double*>(pinned_pool_get(n * sizeof(double), &cap_));
+    }
+    n_ = n;
+    std::fill(p_, p_ + n, v);
+  }
+  double* data() const { return p_; }
+  size_t size() const { return n_; }
+  double* begin() const { return p_; }
+  double* end() const { return p_ + n_; }
+  double& operator[](size_t i) const { return p_[i]; }
+
+ private:
+  double* p_ = nullptr;
+  size_t n_ = 0, cap_ = 0;
 };
 
 template <class T>
@@ -276,7 +311,7 @@ class Solver {
   std::vector<pdlp_step_log_entry> step_log_;
   std::vector<pdlp_restart_event> restart_log_;
   pdlp_result_info info_{};
-  std::vector<double> rx_, ry_, rlam_;
+  PinnedVec rx_, ry_, rlam_;
 
   // ---- sharding (world_ == 1: a single device) ----
   int64_t l2_window_bytes_ = 0;  // persisting L2 carve-out for the gathered iterate

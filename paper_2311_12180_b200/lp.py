@@ -260,11 +260,30 @@ class SolverParams:
         return p
 
 
-@dataclass
 class ReducedCosts:
-    lambda_: np.ndarray
-    lambda_pos: np.ndarray
-    lambda_neg: np.ndarray
+    """ReducedCosts (lp_model.hpp:147-176): lambda and its positive / negative
+    parts. The parts are formed from lambda on first use (two fewer n-vectors
+    to copy out of every solve)."""
+
+    def __init__(self, lambda_: np.ndarray, lambda_pos: np.ndarray | None = None,
+                 lambda_neg: np.ndarray | None = None):
+        self.lambda_ = lambda_
+        self._pos, self._neg = lambda_pos, lambda_neg
+
+    @property
+    def lambda_pos(self) -> np.ndarray:
+        if self._pos is None:
+            self._pos = np.where(self.lambda_ > 0.0, self.lambda_, 0.0)
+        return self._pos
+
+    @property
+    def lambda_neg(self) -> np.ndarray:
+        if self._neg is None:
+            self._neg = np.where(self.lambda_ < 0.0, -self.lambda_, 0.0)
+        return self._neg
+
+    def __repr__(self) -> str:
+        return f"ReducedCosts(n={len(self.lambda_)})"
 
 
 @dataclass
