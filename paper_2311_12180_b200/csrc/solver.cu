@@ -566,8 +566,8 @@ void Solver::precondition() {
   DevBuf<double> part(nb);
   launch_block_absmax(k_val_.get(), nnz_, part.get(), nb, s);
   std::vector<double> ph(nb);
-  d1_.resize(m_);
-  d2_.resize(n_);
+  d1_.resize(size_t(m_));
+  d2_.resize(size_t(n_));
   PDLP_CUDA(cudaMemcpyAsync(ph.data(), part.get(), nb * sizeof(double), cudaMemcpyDeviceToHost, s));
   if (m_)
     PDLP_CUDA(cudaMemcpyAsync(d1_.data(), d1_dev_.get(), m_ * sizeof(double),
@@ -1217,9 +1217,10 @@ void Solver::finish(int status, int slot_x, int slot_y, int slot_lam, const KktH
                     const std::string& msg) {
   const DevState& st = *hs_;
   cudaStream_t s = stream_;
-  rx_.assign(n_, 0.0);
-  ry_.assign(m_, 0.0);
-  rlam_.assign(n_, 0.0);
+  // overwritten below by the D2H copies; zero vectors where no slot supplies one
+  if (slot_x >= 0) rx_.resize(size_t(n_)); else rx_.assign(size_t(n_), 0.0);
+  if (slot_y >= 0) ry_.resize(size_t(m_)); else ry_.assign(size_t(m_), 0.0);
+  rlam_.resize(size_t(n_));
   // the returned point is one slot of the interleaved [.][4] evaluation
   // arrays: extract it on the device (a pitched 8-byte-wide D2H copy costs
   // milliseconds at n = 1e6), then contiguous copies after the device clock

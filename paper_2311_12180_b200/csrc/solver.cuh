@@ -90,12 +90,15 @@ class PinnedVec {
   ~PinnedVec() {
     if (p_) pinned_pool_put(p_, cap_);
   }
-  void assign(size_t n, double v) {
-    if (n * sizeof(double) > cap_) {
+  void resize(size_t n) {  // contents unspecified (the caller overwrites them)
+    if (n * sizeof(double) > cap_ || !p_) {
       if (p_) pinned_pool_put(p_, cap_);
-      p_ = static_cast<double*>(pinned_pool_get(n * sizeof(double), &cap_));
+      p_ = static_cast<double*>(pinned_pool_get(std::max<size_t>(n, 1) * sizeof(double), &cap_));
     }
     n_ = n;
+  }
+  void assign(size_t n, double v) {
+    resize(n);
     std::fill(p_, p_ + n, v);
   }
   double* data() const { return p_; }
@@ -246,7 +249,8 @@ class Solver {
   double objective_constant_ = 0.0;
 
   // host copies of the original vectors (evaluation bookkeeping is host-side)
-  std::vector<double> c_, q_, l_, u_, d1_, d2_;
+  std::vector<double> c_, q_, l_, u_;
+  PinnedVec d1_, d2_;  // the scaling, downloaded once at setup
   double rhs_norm_ = 0.0, obj_norm_ = 0.0;  // termination_norms (solver.hpp:157-163)
   double eta_hat0_ = 1.0, omega0_ = 1.0;
 
