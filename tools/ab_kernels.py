@@ -21,7 +21,8 @@ from paper_2311_12180_b200 import Solver, SolverParams, generators
 lp = generators.config(os.environ["CFG"])
 s = Solver(lp, SolverParams(engine=int(os.environ.get("AB_ENGINE", "0"))))
 r = s.solve(); r = s.solve()
-out = {"iters": r.iterations, "solve_ms": r.info["device_seconds"] * 1e3}
+out = {"iters": r.iterations, "solve_ms": r.info["device_seconds"] * 1e3,
+       "eval_ms": r.info["eval_seconds"] * 1e3, "window_ms": r.info["window_seconds"] * 1e3}
 for which, name in ((2, "K"), (3, "KT"), (0, "dual"), (1, "primal")):
     ms, by = s.time_kernel(which, 200)
     out[name] = round(ms * 1e3, 2)
