@@ -11,7 +11,8 @@ prefixed "<name>/": the CSR, b, c; spectral_norm(A, 1e-12, 100000); the trace
 of restarted_pdhg_standard with s = 0.9 / (2 ||A||), beta 0.5 (epoch start
 KKT values, lengths, counters, last epoch start, first recorded iterates);
 kkt_error_standard and p_s_norm_squared at seeded random points. Plus the
-already-optimal restart chain of test_standard_form.cpp:112-127.
+already-optimal restart chain of test_standard_form.cpp:112-127, and a
+numerical-failure run (f4 with step 1e150).
 """
 from __future__ import annotations
 
@@ -121,8 +122,18 @@ def main() -> None:
     assert L.ref_standard_pdhg(C.byref(A), P(one), P(one), 0.4, 0.5, -1.0, 10, P(one), P(one), P(kkt),
                                abi.i64ptr(lens), 64, abi.i64ptr(cnt), P(xl), P(yl), None, None, 0) == 0
     out.update({"chain/kkt": kkt[:cnt[0]], "chain/lens": lens[:cnt[0]], "chain/counters": cnt})
+    # numerical failure: f4 with a step far beyond 1 / ||A|| (standard_form.hpp:177-180)
+    off, col, val = csr(3, 5, fixtures()["f4"][2])
+    b4, c4 = np.array(fixtures()["f4"][3]), np.array(fixtures()["f4"][4])
+    A = abi.PdlpCsr(num_rows=3, num_cols=5, nnz=len(val), row_offsets=abi.i64ptr(off),
+                    col_indices=abi.i64ptr(col), values=P(val))
+    kkt, lens, cnt = np.zeros(64), np.zeros(64, np.int64), np.zeros(4, np.int64)
+    xl, yl = np.zeros(5), np.zeros(3)
+    assert L.ref_standard_pdhg(C.byref(A), P(b4), P(c4), 1e150, 0.5, 1e-12, 100000, None, None, P(kkt),
+                               abi.i64ptr(lens), 64, abi.i64ptr(cnt), P(xl), P(yl), None, None, 0) == 0
+    out.update({"fail/kkt": kkt[:cnt[0]], "fail/lens": lens[:cnt[0]], "fail/counters": cnt})
     np.savez_compressed(OUT, **out)
-    print("wrote", OUT, "chain epochs", int(cnt[0]))
+    print("wrote", OUT, "chain epochs", len(out["chain/kkt"]), "failure run", out["fail/counters"])
 
 
 if __name__ == "__main__":

@@ -150,3 +150,21 @@ def test_spectral_norm_of_empty_and_identity():
     assert spectral_norm(diag, 1e-14, 100000) == pytest.approx(3.0, abs=1e-8)
     empty = CsrMatrix(2, 3, np.zeros(3, np.int64), np.zeros(0, np.int64), np.zeros(0))
     assert spectral_norm(empty) == 0.0
+
+
+@pytest.mark.parametrize("parity", [True, False])
+def test_numerical_failure_and_limit_edges(parity):
+    """A step far beyond 1/||A|| diverges to a non-finite iterate: the loop
+    ends with numerical_failure and without counting the failed step
+    (standard_form.hpp:177-180); iteration_limit 0 opens the first epoch only."""
+    lp = instance("f4")
+    tr = restarted_pdhg_standard(lp, StandardPdhgOptions(step_size=1e150, convergence_tol=1e-12,
+                                                         iteration_limit=100000, parity=parity))
+    assert tr.numerical_failure and not tr.converged
+    cnt = G["fail/counters"]  # the reference's run of the same case
+    assert (len(tr.epochs), tr.total_iterations, tr.converged, tr.numerical_failure) == \
+        (cnt[0], cnt[1], bool(cnt[2]), bool(cnt[3]))
+    assert np.array_equal([e.length for e in tr.epochs], G["fail/lens"])
+    tr0 = restarted_pdhg_standard(lp, StandardPdhgOptions(step_size=0.1, iteration_limit=0, parity=parity))
+    assert (tr0.total_iterations, len(tr0.epochs), tr0.converged) == (0, 1, False)
+    assert tr0.epochs[0].start_kkt == pytest.approx(G["f4/kkt"][0], rel=0 if parity else 1e-14)
