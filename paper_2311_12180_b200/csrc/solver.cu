@@ -96,12 +96,6 @@ void validate_input(const pdlp_lp& lp, const pdlp_params& params) {
     throw std::runtime_error("instance exceeds the 32-bit index layout of one device (shard it)");
 }
 
-double seq_norm2(const std::vector<double>& v) {
-  double s = 0.0;
-  for (double x : v) s += x * x;
-  return std::sqrt(s);
-}
-
 }  // namespace
 
 double KktHost::weighted(double omega) const {  // KktResiduals::weighted
@@ -581,10 +575,18 @@ void Solver::precondition() {
   eta_hat0_ = mx > 0.0 ? 1.0 / mx : 1.0;
   // initialize_primal_weight on the scaled problem (solver.hpp:293-300, :774-776):
   // the scaled vectors are the same products the device formed.
-  std::vector<double> cs(n_), qs(m_);
-  for (int64_t j = 0; j < n_; ++j) cs[j] = c_[j] * d2_[j];
-  for (int64_t i = 0; i < m_; ++i) qs[i] = q_[i] * d1_[i];
-  const double cn2 = seq_norm2(cs), qn2 = seq_norm2(qs);
+  // norm2 of the scaled c and q, summed in index order as norm2 of the
+  // materialised vectors would be (no n-vector temporaries on the host)
+  double sc = 0.0, sq = 0.0;
+  for (int64_t j = 0; j < n_; ++j) {
+    const double v = c_[j] * d2_[j];
+    sc += v * v;
+  }
+  for (int64_t i = 0; i < m_; ++i) {
+    const double v = q_[i] * d1_[i];
+    sq += v * v;
+  }
+  const double cn2 = std::sqrt(sc), qn2 = std::sqrt(sq);
   const double w = (cn2 > params_.eps_zero && qn2 > params_.eps_zero) ? cn2 / qn2 : 1.0;
   omega0_ = sclamp(w, params_.omega_min, params_.omega_max);
 }
