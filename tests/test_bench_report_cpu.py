@@ -109,3 +109,11 @@ def test_cpp_header_report_matches_reference(probe, tmp_path):
                            for r in GOLD["records"]))
     out = subprocess.run([str(probe), "report", str(tsv), "60"], capture_output=True, text=True, check=True).stdout
     assert out == GOLD["report"]
+
+
+def test_acceptance_criterion_8_hand_values():
+    """acceptance_main.cpp:505-520: SGM10 of [10, 90] and the time-limit
+    contribution of an inconclusive record."""
+    assert abs(B.shifted_geometric_mean([10.0, 90.0], 10.0) - 34.7214) <= 1e-3
+    unsolved = B.BenchmarkRecord(instance="u", status=SolveStatus.TIME_LIMIT, solve_seconds=123.0)
+    assert B.aggregation_time(unsolved, 77.0) == 77.0
