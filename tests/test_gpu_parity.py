@@ -270,6 +270,20 @@ def test_split_rows_deterministic_across_runs():
     assert len(pers) == 1, pers
 
 
+def test_two_suite_runs_bitwise_identical():
+    """acceptance criterion 9 (acceptance_main.cpp:522-544) in fast mode: every
+    suite instance solved twice gives the same status, iteration count, point
+    and objective bit for bit."""
+    p = SolverParams(eps_optimal=1e-8, iteration_limit=200000)
+    for name in suite_names():
+        lp = load_golden_lp(name)
+        a, b = solve(lp, p), solve(lp, p)
+        assert (a.status, a.iterations) == (b.status, b.iterations), name
+        assert sha(a.point.primal, a.point.dual) == sha(b.point.primal, b.point.dual), name
+        assert a.info["primal_objective"] == b.info["primal_objective"] or \
+            (np.isnan(a.info["primal_objective"]) and np.isnan(b.info["primal_objective"])), name
+
+
 def test_graph_and_stream_engines_bitwise():
     """Same per-trial kernels, replayed by a CUDA graph or launched one by one."""
     lp = generators.config("C1")
