@@ -41,6 +41,24 @@ struct DevState {
   unsigned ctr_eval;
   int32_t window_cont;  // set by the window kernel's decision: run another trial
   int32_t pad2;
+  // ---- window chaining (graph engine, fast mode; chain_decide_kernel) ----
+  double kkt_epoch_start;  // the host's restart-test values, mirrored for the device
+  double kkt_last;
+  int32_t chain_left;      // windows the chain may still start after this one
+  int32_t chain_stop;      // 0 running; 1 the last evaluation needs the host; 2 handled
+  int32_t chain_evals;     // evaluations decided on the device in this chain
+  int32_t pad3;
+};
+
+// Constants of the evaluation block's decisions (SolverParams and the
+// instance's termination norms), for the device-side chain decision.
+struct ChainConsts {
+  double eps_optimal, eps_infeasible, eps_zero;
+  double beta_sufficient, beta_necessary, beta_artificial;
+  double rhs_norm, obj_norm;
+  int64_t iteration_limit;
+  int32_t freq;
+  int32_t pad;
 };
 
 // Results of one evaluation block (evaluate_candidates + the infeasibility

@@ -277,6 +277,80 @@ __global__ void __launch_bounds__(kThreads, 4) dual_kernel(DevCsr K, DevIter it,
   if (use_cond) cudaGraphSetConditional(cond, d.cont ? 1u : 0u);
 }
 
+// ---------------------------------------------------------------------------
+// Chained windows: the evaluation block's decision (solver.cu evaluation_block,
+// solver.hpp:843-892) with the host's exact arithmetic (IEEE sqrt and the same
+// operation order, --fmad=false), so the device continues exactly when the
+// host would have found nothing to do.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double chain_weighted(double prn, double drn, double pobj, double dobj, double omega) {
+  const double pr = omega * prn, dr = drn / omega, g = dobj - pobj;  // KktHost::gap
+  return sqrt(pr * pr + dr * dr + g * g);
+}
+
+__device__ __forceinline__ bool chain_terminated(double prn, double drn, double pobj, double dobj,
+                                                 const ChainConsts& k) {
+  if (!isfinite(prn) || !isfinite(drn) || !isfinite(pobj) || !isfinite(dobj)) return false;
+  const double eps = k.eps_optimal;
+  const bool gap_ok = fabs(dobj - pobj) <= eps * (1.0 + fabs(dobj) + fabs(pobj));
+  const bool p_ok = prn <= eps * (1.0 + k.rhs_norm);
+  const bool d_ok = drn <= eps * (1.0 + k.obj_norm);
+  return gap_ok && p_ok && d_ok;
+}
+
+__global__ void chain_decide_kernel(DevState* st, const EvalOut* e, ChainConsts k,
+                                    cudaGraphConditionalHandle outer, cudaGraphConditionalHandle inner) {
+  if (threadIdx.x != 0) return;
+  bool stop = st->failure != 0;
+  double kkt_cand = 0.0;
+  if (!stop) {
+    const double w = st->omega;
+    const double kc = chain_weighted(e->prn[0], e->drn[0], e->pobj[0], e->dobj[0], w);
+    const double ka = chain_weighted(e->prn[1], e->drn[1], e->pobj[1], e->dobj[1], w);
+    const int cand = !(kc < ka) ? 1 : 0;
+    kkt_cand = cand ? ka : kc;
+    stop = chain_terminated(e->prn[cand], e->drn[cand], e->pobj[cand], e->dobj[cand], k) ||
+           chain_terminated(e->prn[1 - cand], e->drn[1 - cand], e->pobj[1 - cand], e->dobj[1 - cand], k);
+    for (int r = 0; r < 2 && !stop; ++r) {
+      const double yn = e->y_norm[r];
+      if (yn > k.eps_zero && e->kty_resid[r] <= k.eps_infeasible * yn && e->ray_dobj[r] > k.eps_infeasible * yn)
+        stop = true;
+      const double xn = e->x_norm[r];
+      if (!stop && xn > k.eps_zero) {
+        const double tol = k.eps_infeasible * xn;
+        if (e->ax_norm[r] <= tol && !(e->gx_negmax[r] > tol) && !(e->xl_negmax[r] > tol) &&
+            !(e->xu_max[r] > tol) && e->cx[r] < -tol)
+          stop = true;
+      }
+    }
+    if (!stop) {  // should_restart: any criterion sends the evaluation to the host
+      if (kkt_cand <= k.beta_sufficient * st->kkt_epoch_start)
+        stop = true;
+      else if (kkt_cand <= k.beta_necessary * st->kkt_epoch_start && kkt_cand > st->kkt_last)
+        stop = true;
+      else if (double(st->inner) >= k.beta_artificial * double(st->total))
+        stop = true;
+    }
+  }
+  if (stop) {
+    st->chain_stop = 1;
+    cudaGraphSetConditional(outer, 0u);
+    return;
+  }
+  st->kkt_last = kkt_cand;
+  st->chain_evals += 1;
+  if (st->chain_left > 0 && st->total + k.freq <= k.iteration_limit) {
+    st->chain_left -= 1;
+    st->window_accepts = 0;
+    st->window_target = k.freq;
+    cudaGraphSetConditional(inner, 1u);
+    cudaGraphSetConditional(outer, 1u);
+  } else {
+    st->chain_stop = 2;
+    cudaGraphSetConditional(outer, 0u);
+  }
+}
+
 // ===========================================================================
 // Iteration: primal kernel
 // ===========================================================================
@@ -1468,6 +1542,13 @@ void launch_eval(const DevCsr& k, const DevCsr& kt, const DevIter& it, const Dev
     eval_reduce_kernel<<<kEvalReduceCtas, kThreads, 0, s>>>(ev);
     eval_final_kernel<false><<<1, kThreads, 0, s>>>(ev, ev.ev1_tiles, ev.ev2_tiles, it.n, it.m, it.m1);
   }
+  PDLP_CUDA(cudaGetLastError());
+}
+
+void launch_chain_decide(DevState* st, const EvalOut* e, const ChainConsts& k, unsigned long long outer,
+                         unsigned long long inner, cudaStream_t s) {
+  chain_decide_kernel<<<1, 32, 0, s>>>(st, e, k, static_cast<cudaGraphConditionalHandle>(outer),
+                                       static_cast<cudaGraphConditionalHandle>(inner));
   PDLP_CUDA(cudaGetLastError());
 }
 

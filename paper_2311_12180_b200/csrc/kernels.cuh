@@ -63,6 +63,12 @@ void launch_dual(const DevCsr& k, const DevIter& it, bool seq, unsigned long lon
                  int use_cond, cudaStream_t s);
 // Separate step decision (it.decide_sep): sums the dual partials once.
 void launch_decide(const DevIter& it, cudaStream_t s, unsigned long long cond = 0, int use_cond = 0);
+// The evaluation block's decision on the device for chained windows: when the
+// evaluation neither terminates, certifies infeasibility nor restarts, records
+// kkt_last and starts the next window (outer / inner WHILE conditions);
+// otherwise stops the chain for the host (Solver::evaluation_block).
+void launch_chain_decide(DevState* st, const EvalOut* e, const ChainConsts& k, unsigned long long outer,
+                         unsigned long long inner, cudaStream_t s);
 // Primal side: K'y' + average + next trial x' (mode from state, or forced).
 void launch_primal(const DevCsr& kt, const DevIter& it, bool seq, int mode_override,
                    cudaStream_t s, unsigned long long cond = 0, int use_cond = 0);

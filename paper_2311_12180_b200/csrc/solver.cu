@@ -142,6 +142,8 @@ Solver::~Solver() {
   if (fork_.s2) cudaStreamDestroy(fork_.s2);
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
   if (graph_) cudaGraphDestroy(graph_);
+  if (chain_exec_) cudaGraphExecDestroy(chain_exec_);
+  if (chain_graph_) cudaGraphDestroy(chain_graph_);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -647,13 +649,21 @@ void Solver::allocate_iteration() {
   seq_inter_.alloc(seq ? m_ : 1);
   seq_dx2_.alloc(seq ? n_ : 1);
   tab_cap_ = int(std::min<int64_t>(params_.evaluation_frequency, 4096));
+  // chained windows (graph engine, fast mode, one rank, no step log): up to
+  // 16 windows per launch, the device deciding the evaluations in between
+  chain_windows_ = 0;
+  if (!parity() && world_ == 1 && !params_.record_step_log && params_.evaluation_frequency <= 1024 &&
+      (params_.engine == PDLP_ENGINE_GRAPH || (params_.engine == PDLP_ENGINE_AUTO && params_.use_cuda_graph)) &&
+      !std::getenv("PDLP_NO_CHAIN"))
+    chain_windows_ = 16;
   {
     // [EvalOut | DevState | step-factor pairs]: one D2H (eval + state) and one
     // H2D (state + factors) per window round trip
     auto up64 = [](size_t b) { return (b + 63) & ~size_t(63); };
     xo_state_ = up64(sizeof(EvalOut));
     xo_tab_ = xo_state_ + up64(sizeof(DevState));
-    const size_t bytes = xo_tab_ + 2 * sizeof(double) * size_t(std::max(tab_cap_, 128));  // head stages 128
+    const size_t tab_entries = size_t(std::max(tab_cap_ * std::max(chain_windows_, 1), 128));  // head stages 128
+    const size_t bytes = xo_tab_ + 2 * sizeof(double) * tab_entries;
     xfer_dev_.alloc(bytes);
     xfer_dev_.zero(s);
     xfer_host_.alloc(bytes);
@@ -861,6 +871,110 @@ void Solver::capture_window_graph() {
   cond_handle_ = static_cast<unsigned long long>(h);
 }
 
+// WHILE(chain) { WHILE(window) { dual; primal }; evaluation; chain decision }.
+// The inner body is the same capture as capture_window_graph; the outer body
+// adds the evaluation block of launch_eval and chain_decide_kernel, which
+// either re-arms both conditions for the next window or ends the chain.
+void Solver::capture_chain_graph() {
+  PDLP_CUDA(cudaGraphCreate(&chain_graph_, 0));
+  cudaGraphConditionalHandle ho, hi;
+  PDLP_CUDA(cudaGraphConditionalHandleCreate(&ho, chain_graph_, 1, cudaGraphCondAssignDefault));
+  PDLP_CUDA(cudaGraphConditionalHandleCreate(&hi, chain_graph_, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams op = {};
+  op.type = cudaGraphNodeTypeConditional;
+  op.conditional.handle = ho;
+  op.conditional.type = cudaGraphCondTypeWhile;
+  op.conditional.size = 1;
+  cudaGraphNode_t onode;
+  PDLP_CUDA(cudaGraphAddNode(&onode, chain_graph_, nullptr, 0, &op));
+  cudaGraph_t obody = op.conditional.phGraph_out[0];
+  cudaGraphNodeParams ip = {};
+  ip.type = cudaGraphNodeTypeConditional;
+  ip.conditional.handle = hi;
+  ip.conditional.type = cudaGraphCondTypeWhile;
+  ip.conditional.size = 1;
+  cudaGraphNode_t inode;
+  PDLP_CUDA(cudaGraphAddNode(&inode, obody, nullptr, 0, &ip));
+  cudaGraph_t ibody = ip.conditional.phGraph_out[0];
+  const unsigned long long ci = static_cast<unsigned long long>(hi), co = static_cast<unsigned long long>(ho);
+  // inner body: one trial (as capture_window_graph)
+  PDLP_CUDA(cudaStreamBeginCaptureToGraph(stream_, ibody, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  const int ds = it_.decide_sep;
+  dual_step(ci, ds == 2 ? 1 : 0);
+  if (ds == 1) launch_decide(it_, stream_, ci, 1);
+  primal_step(-1, ci, ds == 0 ? 1 : 0);
+  PDLP_CUDA(cudaStreamEndCapture(stream_, &ibody));
+  // outer body after the inner loop: evaluation + decision
+  PDLP_CUDA(cudaStreamBeginCaptureToGraph(stream_, obody, &inode, nullptr, 1, cudaStreamCaptureModeThreadLocal));
+  launch_eval(k_ev_.csr, kt_ev_.csr, it_, ev_, false, stream_, phase_, fork_.s2 ? &fork_ : nullptr);
+  ChainConsts k{};
+  k.eps_optimal = params_.eps_optimal;
+  k.eps_infeasible = params_.eps_infeasible;
+  k.eps_zero = params_.eps_zero;
+  k.beta_sufficient = params_.beta_sufficient;
+  k.beta_necessary = params_.beta_necessary;
+  k.beta_artificial = params_.beta_artificial;
+  k.rhs_norm = rhs_norm_;
+  k.obj_norm = obj_norm_;
+  k.iteration_limit = params_.iteration_limit;
+  k.freq = int32_t(params_.evaluation_frequency);
+  launch_chain_decide(state_dev_, eval_dev_, k, co, ci, stream_);
+  PDLP_CUDA(cudaStreamEndCapture(stream_, &obody));
+  PDLP_CUDA(cudaGraphInstantiate(&chain_exec_, chain_graph_, 0));
+}
+
+bool Solver::chain_enabled() const {
+  return chain_windows_ > 1 && engine_ == PDLP_ENGINE_GRAPH;
+}
+
+// Up to `windows` full windows with the evaluations between them decided on
+// the device. Returns true when the chain ended on a device-decided
+// evaluation (nothing left for evaluation_block), false when the last
+// evaluation needs the host (termination, infeasibility, restart) or a window
+// failed.
+bool Solver::run_chain(int windows) {
+  DevState& st = *hs_;
+  const int freq = int(params_.evaluation_frequency);
+  double* tab = tab_host_;
+  const int steps = windows * freq;
+  for (int i = 0; i < steps; ++i) {
+    const double kp1 = double(st.total + 1 + i) + 1.0;
+    tab[2 * i] = 1.0 - std::pow(kp1, -params_.step_reduction_exponent);
+    tab[2 * i + 1] = 1.0 + std::pow(kp1, -params_.step_growth_exponent);
+  }
+  st.window_target = freq;
+  st.window_accepts = 0;
+  st.table_base = st.total;
+  st.failure = 0;
+  st.kkt_epoch_start = kkt_epoch_start_;
+  st.kkt_last = kkt_last_;
+  st.chain_left = windows - 1;
+  st.chain_stop = 0;
+  st.chain_evals = 0;
+  const int64_t trials_before = st.trials_total;
+  PDLP_CUDA(cudaMemcpyAsync(state_dev_, hs_, xo_tab_ - xo_state_ + 2 * sizeof(double) * size_t(steps),
+                            cudaMemcpyHostToDevice, stream_));
+  eval_fresh_ = false;
+  PDLP_CUDA(cudaEventRecord(ev_w0_, stream_));
+  if (!chain_exec_) capture_chain_graph();
+  PDLP_CUDA(cudaGraphLaunch(chain_exec_, stream_));
+  PDLP_CUDA(cudaEventRecord(ev_w1_, stream_));
+  PDLP_CUDA(cudaEventRecord(ev_e1_, stream_));
+  PDLP_CUDA(cudaMemcpyAsync(he_, eval_dev_, xo_state_ + sizeof(DevState), cudaMemcpyDeviceToHost, stream_));
+  spin_sync();
+  eval_fresh_ = true;
+  {
+    float ms = 0.f;
+    PDLP_CUDA(cudaEventElapsedTime(&ms, ev_w0_, ev_w1_));
+    window_seconds_ += 1e-3 * double(ms);  // windows and their evaluations
+  }
+  const int evals = st.chain_evals + (st.chain_stop == 1 ? 1 : 0);
+  evaluations_ += evals;
+  launches_ += int64_t(evals) * 6 + (it_.decide_sep == 1 ? 3 : 2) * (st.trials_total - trials_before);
+  kkt_last_ = st.kkt_last;
+  return st.chain_stop == 2;
+}
+
 void Solver::upload_state() {
   PDLP_CUDA(cudaMemcpyAsync(state_dev_, hs_, sizeof(DevState), cudaMemcpyHostToDevice,
                             stream_));
@@ -968,6 +1082,24 @@ void Solver::iterate_run(int64_t count, int32_t* status) {
     target = std::min<int64_t>(target, count - done);
     target = std::min<int64_t>(target, tab_cap_);
     const int64_t before = st.total;
+    if (chain_enabled() && target == freq && st.inner % freq == 0 &&
+        count - done >= int64_t(freq) * chain_windows_ &&
+        params_.time_limit_seconds - elapsed() > 1.0) {
+      // whole windows back to back on the device; the host sees only the
+      // evaluation that needs it (or the chain's end)
+      const int64_t fit = (params_.iteration_limit - st.total) / freq;
+      const int w = int(std::min<int64_t>(chain_windows_, fit));
+      const bool handled = run_chain(w);
+      done += st.total - before;
+      if (st.failure) {
+        evaluate();
+        finish_candidate(PDLP_STATUS_NUMERICAL_ERROR,
+                         "non-finite iterate in adaptive step at iteration " + std::to_string(st.total));
+        break;
+      }
+      if (!handled) evaluation_block();
+      continue;
+    }
     run_window(int(target));
     done += st.total - before;
     if (st.failure) {

@@ -229,6 +229,9 @@ class Solver {
   void allocate_iteration();
   void pin_iterates_in_l2();
   void capture_window_graph();
+  void capture_chain_graph();
+  bool chain_enabled() const;
+  bool run_chain(int windows);  // true: the last evaluation was decided on the device
   void upload_state();
   void download_state();
   void spin_sync();
@@ -291,6 +294,10 @@ class Solver {
   cudaGraph_t graph_ = nullptr;
   cudaGraphExec_t graph_exec_ = nullptr;
   unsigned long long cond_handle_ = 0;
+  // chained windows: WHILE(chain) { WHILE(window) { dual; primal }; evaluation; decision }
+  cudaGraph_t chain_graph_ = nullptr;
+  cudaGraphExec_t chain_exec_ = nullptr;
+  int chain_windows_ = 0;  // windows per chain launch (0: chaining off)
 
   // host-side loop state (solver.hpp:683-698)
   int64_t outer_ = 0;

@@ -284,6 +284,28 @@ def test_two_suite_runs_bitwise_identical():
             (np.isnan(a.info["primal_objective"]) and np.isnan(b.info["primal_objective"])), name
 
 
+@pytest.mark.parametrize("which", ["C1", "transport", "skewed", "staircase", "infeasible_primal", "rand07",
+                                   "C1_limit"])
+def test_chained_windows_bitwise_equal_to_host_decided(which, monkeypatch):
+    """Windows chained on the device (the evaluation's no-restart decision
+    taken by chain_decide_kernel) give the same solve as the host deciding
+    after every window: status, iteration and restart counts, restart log,
+    point and objective, bit for bit."""
+    lp = {"C1": lambda: generators.config("C1"), "C1_limit": lambda: generators.config("C1"),
+          "transport": lambda: generators.transport_lp(60, 80, seed=11), "skewed": skewed_lp,
+          "staircase": lambda: generators.staircase_lp(3, 2000, 500, 500, seed=8)}.get(
+              which, lambda: load_golden_lp(which))()
+    p = SolverParams(eps_optimal=1e-8, iteration_limit=1000 if which == "C1_limit" else 400000)
+    a = solve(lp, p)
+    monkeypatch.setenv("PDLP_NO_CHAIN", "1")
+    b = solve(lp, p)
+    assert (a.status, a.iterations, a.restarts) == (b.status, b.iterations, b.restarts), which
+    assert np.array_equal(a.restart_log, b.restart_log)
+    assert sha(a.point.primal, a.point.dual, a.reduced.lambda_) == sha(b.point.primal, b.point.dual, b.reduced.lambda_)
+    assert a.info["primal_objective"] == b.info["primal_objective"] or np.isnan(a.info["primal_objective"])
+    assert a.info["evaluations"] == b.info["evaluations"]
+
+
 def test_graph_and_stream_engines_bitwise():
     """Same per-trial kernels, replayed by a CUDA graph or launched one by one."""
     lp = generators.config("C1")
