@@ -967,6 +967,8 @@ bool Solver::run_chain(int windows) {
     float ms = 0.f;
     PDLP_CUDA(cudaEventElapsedTime(&ms, ev_w0_, ev_w1_));
     window_seconds_ += 1e-3 * double(ms);  // windows and their evaluations
+    const int ran = windows - st.chain_left;
+    if (ran > 0) window_time_est_ = 1e-3 * double(ms) / double(ran);
   }
   const int evals = st.chain_evals + (st.chain_stop == 1 ? 1 : 0);
   evaluations_ += evals;
@@ -1082,13 +1084,15 @@ void Solver::iterate_run(int64_t count, int32_t* status) {
     target = std::min<int64_t>(target, count - done);
     target = std::min<int64_t>(target, tab_cap_);
     const int64_t before = st.total;
+    // a chain may use half of the remaining time limit, at the measured window rate
+    const double left = params_.time_limit_seconds - elapsed();
+    const int64_t by_time = window_time_est_ > 0.0 ? int64_t(0.5 * left / window_time_est_) : 0;
     if (chain_enabled() && target == freq && st.inner % freq == 0 &&
-        count - done >= int64_t(freq) * chain_windows_ &&
-        params_.time_limit_seconds - elapsed() > 1.0) {
+        count - done >= int64_t(freq) * chain_windows_ && by_time >= 2) {
       // whole windows back to back on the device; the host sees only the
       // evaluation that needs it (or the chain's end)
       const int64_t fit = (params_.iteration_limit - st.total) / freq;
-      const int w = int(std::min<int64_t>(chain_windows_, fit));
+      const int w = int(std::min<int64_t>(std::min<int64_t>(chain_windows_, fit), by_time));
       const bool handled = run_chain(w);
       done += st.total - before;
       if (st.failure) {
@@ -1181,8 +1185,10 @@ void Solver::run_window(int target) {
     float ms = 0.f;
     PDLP_CUDA(cudaEventElapsedTime(&ms, ev_w0_, ev_w1_));
     window_seconds_ += 1e-3 * double(ms);
-    PDLP_CUDA(cudaEventElapsedTime(&ms, ev_w1_, ev_e1_));
-    eval_seconds_ += 1e-3 * double(ms);
+    float ems = 0.f;
+    PDLP_CUDA(cudaEventElapsedTime(&ems, ev_w1_, ev_e1_));
+    eval_seconds_ += 1e-3 * double(ems);
+    if (target == int(params_.evaluation_frequency)) window_time_est_ = 1e-3 * double(ms + ems);
   }
   if (engine_ != PDLP_ENGINE_PERSISTENT)
     launches_ += (it_.decide_sep == 1 ? 3 : 2) * (st.trials_total - trials_before);

@@ -298,6 +298,7 @@ class Solver {
   cudaGraph_t chain_graph_ = nullptr;
   cudaGraphExec_t chain_exec_ = nullptr;
   int chain_windows_ = 0;  // windows per chain launch (0: chaining off)
+  double window_time_est_ = 0.0;  // measured seconds per window (bounds a chain by the time limit)
 
   // host-side loop state (solver.hpp:683-698)
   int64_t outer_ = 0;
