@@ -1009,6 +1009,10 @@ double Solver::elapsed() const {
 void Solver::iterate_begin(int32_t* status) {
   PDLP_CUDA(cudaSetDevice(params_.device));
   require_linked();
+  // graphs are captured and instantiated once per handle, before the solve's
+  // clocks start (the first instantiation in a process also loads the modules)
+  if (engine_ == PDLP_ENGINE_GRAPH && !graph_exec_) capture_window_graph();
+  if (chain_enabled() && !chain_exec_) capture_chain_graph();
   t0_ = std::chrono::steady_clock::now();
   DevState& st = *hs_;
   std::memset(&st, 0, sizeof st);
