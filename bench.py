@@ -1,23 +1,29 @@
 #!/usr/bin/env python3
-"""Benchmark: restarted-PDHG iterations/s on BASELINE.json configs[1] (C2:
-synthetic 1000 x 1000 transportation LP, n = 1e6, m = 2000, nnz = 2e6, solved
-from z = 0 to 1e-4 relative KKT).
+"""Benchmark: restarted-PDHG iterations/s and time to 1e-4 relative KKT on
+BASELINE.json configs[3] (C4: synthetic random sparse LP, m = 2e7 rows
+(1e7 inequalities + 1e7 equalities), n = 4e7 columns, 5 nonzeros per column,
+nnz = 2e8, fp64), the largest configuration one B200 holds. C2 (configs[1],
+the 1k x 1k transportation LP, to 1e-4 and 1e-8) is reported beside it.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-A step is one complete solve on the device-resident instance (the reference's
-solve_seconds scope, solver.hpp:636-646,760). `value` = total PDHG iterations of
-all ranks / max-over-ranks device time of the K timed solves (CUDA events on the
-solver's stream, inside libpdlp_b200). `e2e` = the same metric through the
-C-ABI with host buffers: pdlp_create (H2D, K^T build, preconditioning) +
-pdlp_solve + pdlp_get_solution (D2H) every step. C2 fits one GPU many times
-over and does not shard ("C1 and C2 ... run them as replicas
-only"), so N > 1 runs N independent replicas (weak scaling, no collective on the
-data path). L2 (126 MB) is flushed between timed solves with a 256 MiB write.
+A step is one complete solve of the device-resident instance from z = 0 to
+1e-4 relative KKT (the reference's solve_seconds scope, solver.hpp:636-646,
+760). `value` = PDHG iterations of all ranks / max-over-ranks device time of
+the K timed solves (CUDA events on the solver's stream, inside libpdlp_b200).
+`e2e` = the same metric through the C-ABI with host buffers: pdlp_create
+(H2D of the 2.4 GB instance, K^T build, preconditioning, panel plans) +
+pdlp_solve + pdlp_get_solution (D2H of x, y, lambda) every step. The inputs
+(> 4 GB) exceed the 126 MB L2; L2 is also flushed between timed solves.
+N > 1: every rank solves its own replica on its own GPU (weak scaling, no
+collective on the data path).
 
---impl reference times the reference CPU solver (oracle/_ref, the unmodified
-pdhglp headers compiled in place) on the host cores: one solve per core, each a
-bounded iteration sample of the same instance; rank 0 only.
+--impl reference times the reference CPU solver (oracle/_ref: the unmodified
+pdhglp headers compiled in place) on the host cores: one shared setup of the
+same C4 instance (SolveLoop's scaling and saddle form), then one concurrent
+solve per core (forked iterate states), each step a bounded iteration sample;
+rank 0 only. The reference cannot reach 1e-4 on C4 in bench time (about 5 s
+per iteration on one core), so the metric there is iterations/s.
 """
 from __future__ import annotations
 
@@ -38,8 +44,11 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "PDHG iters/sec (solve to 1e-4 relative KKT)"
 UNIT = "iter/s"
-WORKLOAD = "C2 synthetic transportation LP 1000 sources x 1000 sinks (n=1,000,000, m=2,000, nnz=2,000,000), fp64, z0=0 to 1e-4 relative KKT"
-CPU_SAMPLE_ITERS = 384
+CONFIG = "C4"
+WORKLOAD = ("C4 synthetic random sparse LP (BASELINE configs[3]): m=20,000,000 (10M inequality + 10M equality "
+            "rows), n=40,000,000, nnz=200,000,000, boxes [0,10], fp64, z0=0 to 1e-4 relative KKT")
+C2_WORKLOAD = "C2 synthetic transportation LP 1000 x 1000 (n=1,000,000, m=2,000, nnz=2,000,000)"
+E2E_STEPS = 3
 
 
 def env_rank():
@@ -137,40 +146,75 @@ def lp_bytes(lp) -> int:
     return tot
 
 
-def profile_traffic():
-    """Per-launch DRAM traffic of the primal kernel from the committed ncu summary."""
+def profile_traffic(config: str):
+    """Per-launch DRAM traffic (ncu dram__bytes_read + write) of the dual and
+    primal kernel groups of `config` from the committed ncu summary."""
     p = ROOT / "profiles" / "ncu_summary.json"
     if p.exists():
         try:
             d = json.loads(p.read_text())
-            return d.get("primal_kernel", {}).get("dram_bytes_per_launch")
+            return d.get(config, {})
         except Exception:
-            return None
-    return None
+            return {}
+    return {}
 
 
-def cpu_reference_rate(lp, iters: int, threads: int) -> tuple[float, dict]:
-    """The reference solver (oracle/_ref) on `threads` host cores, one
-    independent bounded solve per core; aggregate = sum of per-core rates."""
+def mem_available_gb() -> float:
+    try:
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemAvailable:"):
+                return float(ln.split()[1]) / 1048576.0
+    except OSError:
+        pass
+    return 0.0
+
+
+def reference_sessions(lp, threads: int):
+    """One reference session (setup: make_scaling, apply_scaling, to_saddle)
+    plus threads-1 forks sharing it. Falls back to the C port when the
+    reference harness is not built."""
     from oracle import oracle as O
     from paper_2311_12180_b200 import SolverParams
 
     kind = "ref" if O.available("ref") else "oracle"
-    params = SolverParams(iteration_limit=iters, time_limit_seconds=600.0)
-    rates = [0.0] * threads
+    t = time.perf_counter()
+    s0 = O.Session(lp, SolverParams(iteration_limit=10**9, time_limit_seconds=1e9), kind)
+    setup = time.perf_counter() - t
+    sess = [s0]
+    if kind == "ref":
+        sess += [s0.fork() for _ in range(threads - 1)]
+    return kind, sess, setup
 
-    def work(i):
-        r = O.solve(lp, params, kind)
-        rates[i] = r.iterations / max(r.solve_seconds, 1e-12)
 
-    ts = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
-    for t in ts:
-        t.start()
-    for t in ts:
-        t.join()
-    return float(sum(rates)), {"kind": "reference" if kind == "ref" else "port", "cores": threads,
-                               "sample": f"{iters} iterations of the same C2 instance per core after setup "
-                                         f"(the reference's solve_seconds scope), {threads} concurrent solve(s)"}
+def run_sessions(sess, iters: int) -> float:
+    """Runs `iters` iterations on every session concurrently (ctypes drops the
+    GIL); returns the aggregate iterations/s of the step."""
+    ts = [threading.Thread(target=s.run, args=(iters,)) for s in sess]
+    t = time.perf_counter()
+    for th in ts:
+        th.start()
+    for th in ts:
+        th.join()
+    return len(sess) * iters / (time.perf_counter() - t)
+
+
+def cpu_sample_main(args) -> None:
+    """Child process of our arm: the reference on one host core, on a bounded
+    sample of the bench workload (setup, then --cpu-iters iterations)."""
+    from paper_2311_12180_b200 import generators
+
+    try:
+        os.sched_setaffinity(0, {max(os.sched_getaffinity(0))})
+    except (AttributeError, OSError):
+        pass
+    lp = generators.config(CONFIG)
+    kind, sess, setup = reference_sessions(lp, 1)
+    sess[0].run(1)  # first iteration: page-in of the saddle operators
+    rate = run_sessions(sess, args.cpu_iters)
+    print(json.dumps({"value": rate, "unit": UNIT, "kind": "reference" if kind == "ref" else "port", "cores": 1,
+                      "sample": f"{args.cpu_iters} iterations of the same {CONFIG} instance on 1 core after the "
+                                f"reference's setup ({setup:.0f} s, outside the sample, as solve_seconds)"}),
+          flush=True)
 
 
 def run_reference(args):
@@ -179,25 +223,60 @@ def run_reference(args):
         return
     from paper_2311_12180_b200 import generators
 
-    lp = generators.config("C2")
-    threads = max(1, min(os.cpu_count() or 1, 32))
+    lp = generators.config(CONFIG)
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    # each forked solve holds ~5 (n + m) doubles of iterate state (C4: ~2.4 GB) plus
+    # the step's temporaries; the shared setup ~16 B/nnz per matrix copy
+    per = 8.0 * 10 * (lp.num_variables + lp.num_constraints) / 2**30
+    shared = 8 * 16.0 * lp.nnz / 2**30
+    threads = int(max(1, min(cores, 32, (mem_available_gb() - shared - 8.0) // max(per, 1e-3))))
+    kind, sess, setup = reference_sessions(lp, threads)
+    iters = max(1, args.ref_iters)
     for _ in range(args.warmup):
-        cpu_reference_rate(lp, 16, threads)
-    vals = []
-    desc = None
-    for _ in range(args.steps):
-        v, desc = cpu_reference_rate(lp, args.cpu_iters, threads)
-        vals.append(v)
+        run_sessions(sess, iters)
+    vals = [run_sessions(sess, iters) for _ in range(args.steps)]
+    for s in sess:
+        s.close()
     value = float(np.mean(vals))
+    desc = {"kind": "reference" if kind == "ref" else "port", "cores": threads,
+            "sample": f"{iters} iteration(s) per step on each of {threads} concurrent solves of the same "
+                      f"{CONFIG} instance (one shared reference setup of {setup:.0f} s, outside the timing, "
+                      f"as solve_seconds; forked iterate states)"}
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator)",
-        "config": {"workload": WORKLOAD, "eps": 1e-4, "seed": generators.SEEDS["C2"]},
+        "config": {"workload": WORKLOAD, "eps": 1e-4, "seed": generators.SEEDS[CONFIG]},
         "cpu_baseline": {"value": value, "unit": UNIT, **desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def c2_extra(device: int) -> dict:
+    """C2 (BASELINE configs[1]) beside the headline: device-timed solves to
+    1e-4 and 1e-8 (one warm solve each) and the iteration-kernel timings."""
+    from paper_2311_12180_b200 import Solver, SolverParams, generators
+
+    lp = generators.config("C2")
+    out = {"workload": C2_WORKLOAD}
+    for eps in (1e-4, 1e-8):
+        with Solver(lp, SolverParams(eps_optimal=eps, device=device)) as s:
+            s.solve()
+            r = s.solve()
+            out[f"solve_{eps:g}"] = {"status": str(r.status), "iterations": r.iterations,
+                                     "device_ms": 1e3 * r.info["device_seconds"],
+                                     "it_per_s": r.iterations / r.info["device_seconds"],
+                                     "primal_objective": r.info["primal_objective"]}
+            if eps == 1e-4:
+                for which, name in ((0, "dual"), (1, "primal")):
+                    ms, alg = s.time_kernel(which, 200)
+                    kb = s.kernel_bytes(which)
+                    out[f"{name}_us"] = 1e3 * ms
+                    out[f"{name}_alg_gbs"] = alg / (ms * 1e-3) / 1e9
+                    out[f"{name}_moved_gbs"] = kb["moved"] / (ms * 1e-3) / 1e9
+    out["note"] = "working set ~130 MB: L2-resident across iterations (an L2/latency figure, not HBM)"
+    return out
 
 
 def run_ours(args):
@@ -212,9 +291,19 @@ def run_ours(args):
         dist.init_process_group("nccl")
     device = local if world > 1 else 0
     torch.cuda.set_device(device)
-    from paper_2311_12180_b200 import Solver, SolverParams, SolveStatus, generators
+    from paper_2311_12180_b200 import Solver, SolverParams, generators
 
-    lp = generators.config("C2")
+    # the CPU baseline runs beside the GPU timing in a child process pinned to
+    # the last core (reference setup on C4 takes minutes of host time)
+    cpu_proc = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu_proc = subprocess.Popen([sys.executable, str(ROOT / "bench.py"), "--cpu-sample",
+                                     "--cpu-iters", str(args.cpu_iters)], stdout=subprocess.PIPE,
+                                    stderr=subprocess.PIPE, text=True)
+    t = time.perf_counter()
+    lp = generators.config(CONFIG)
+    gen_s = time.perf_counter() - t
+    n, m, nnz = lp.num_variables, lp.num_constraints, lp.nnz
     params = SolverParams(eps_optimal=1e-4, device=device)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{device}")
 
@@ -223,7 +312,9 @@ def run_ours(args):
         if dist:
             dist.barrier()
 
+    t = time.perf_counter()
     solver = Solver(lp, params)
+    setup_s = time.perf_counter() - t
     for _ in range(args.warmup):
         solver.solve()
     # ---- timed region (device-resident inputs) ----
@@ -255,36 +346,30 @@ def run_ours(args):
     value = total_iters / max_dev_s
     last = results[-1]
 
-    # ---- roofline of the dominant kernel (primal: K'y' fused update) ----
+    # ---- roofline of the dominant kernel group (dual: K x' + update; primal: K'y' + update) ----
     peak, peak_kind = peaks()
-    prim_ms, prim_bytes = solver.time_kernel(1, 200)
-    dual_ms, dual_bytes = solver.time_kernel(0, 200)
-    # time to 1e-8 relative KKT (BASELINE configs[1] quotes both tolerances), one solve
-    with Solver(lp, SolverParams(eps_optimal=1e-8, device=device)) as s8:
-        r8 = s8.solve()
-    tol8 = {"status": str(r8.status), "iterations": r8.iterations, "device_ms": 1e3 * r8.info["device_seconds"],
-            "primal_objective": r8.info["primal_objective"]}
-    # plain SpMV over K and the stored K^T (BASELINE metric: "SpMV GB/s vs HBM peak")
-    spmv = {}
-    for which, name in ((2, "K"), (3, "KT")):
-        ms_, by_ = solver.time_kernel(which, 200)
-        spmv[name] = {"us": 1e3 * ms_, "bytes": by_, "gbs": by_ / (ms_ * 1e-3) / 1e9,
-                      "frac": by_ / (ms_ * 1e-3) / 1e9 / peaks()[0]}
+    kern = {}
+    for which, name in ((0, "dual"), (1, "primal"), (2, "spmv_K"), (3, "spmv_KT")):
+        ms, alg = solver.time_kernel(which, 20)
+        kb = solver.kernel_bytes(which)
+        kern[name] = {"us": 1e3 * ms, "alg_bytes": alg, "moved_bytes": kb["moved"], "panels": kb["panels"],
+                      "alg_gbs": alg / (ms * 1e-3) / 1e9, "moved_gbs": kb["moved"] / (ms * 1e-3) / 1e9}
     solver.close()
-    dom = "primal" if prim_ms >= dual_ms else "dual"
-    ms, by = (prim_ms, prim_bytes) if dom == "primal" else (dual_ms, dual_bytes)
-    achieved = by / (ms * 1e-3) / 1e9
+    dom = "primal" if kern["primal"]["us"] >= kern["dual"]["us"] else "dual"
+    dk = kern[dom]
+    traffic = profile_traffic(CONFIG).get(dom, {})
 
     # ---- e2e through the C-ABI with host buffers ----
+    e2e_steps = max(1, min(args.steps, E2E_STEPS))
     e2e_iters, e2e_s = 0, 0.0
     h2d = lp_bytes(lp)
     d2h = 8 * (2 * lp.num_variables + lp.num_constraints)  # x, y, lambda
     parts = {"create_ms": 0.0, "solve_ms": 0.0, "destroy_ms": 0.0}
-    for _ in range(max(1, args.steps)):
+    for _ in range(e2e_steps):
         flush.fill_(1.0)
         barrier()
         t0 = time.perf_counter()
-        s2 = Solver(lp, params)  # pdlp_create: H2D + K^T + preconditioning
+        s2 = Solver(lp, params)  # pdlp_create: H2D + K^T + preconditioning + plans
         t1 = time.perf_counter()
         r2 = s2.solve()  # pdlp_solve + pdlp_get_solution (D2H)
         t2 = time.perf_counter()
@@ -292,9 +377,9 @@ def run_ours(args):
         torch.cuda.synchronize()
         t3 = time.perf_counter()
         e2e_s += t3 - t0
-        parts["create_ms"] += 1e3 * (t1 - t0) / args.steps
-        parts["solve_ms"] += 1e3 * (t2 - t1) / args.steps
-        parts["destroy_ms"] += 1e3 * (t3 - t2) / args.steps
+        parts["create_ms"] += 1e3 * (t1 - t0) / e2e_steps
+        parts["solve_ms"] += 1e3 * (t2 - t1) / e2e_steps
+        parts["destroy_ms"] += 1e3 * (t3 - t2) / e2e_steps
         e2e_iters += r2.iterations
     et = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{device}")
     ei = torch.tensor([float(e2e_iters)], dtype=torch.float64, device=f"cuda:{device}")
@@ -302,45 +387,51 @@ def run_ours(args):
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
         dist.all_reduce(ei, op=dist.ReduceOp.SUM)
     e2e_value = float(ei.item()) / float(et.item())
+    del lp
+
+    c2 = c2_extra(device) if rank == 0 and not args.no_c2 else None
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        v, desc = cpu_reference_rate(lp, args.cpu_iters, 1)
-        cpu = {"value": v, "unit": UNIT, **desc}
+    if cpu_proc is not None:
+        out, err = cpu_proc.communicate(timeout=1800)
+        try:
+            cpu = json.loads(out.strip().splitlines()[-1])
+        except (ValueError, IndexError):
+            cpu = {"value": None, "unit": UNIT, "kind": "reference", "cores": 1,
+                   "sample": f"failed: {err.strip()[-300:]}"}
 
     if rank == 0:
-        n, m, nnz = lp.num_variables, lp.num_constraints, lp.nnz
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * max_dev_s / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, no dataset)",
-            "config": {"workload": WORKLOAD, "eps": 1e-4, "seed": generators.SEEDS["C2"],
+            "config": {"workload": WORKLOAD, "eps": 1e-4, "seed": generators.SEEDS[CONFIG],
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                       "l2": "flushed between timed solves (256 MiB write); working set ~130 MB"},
+                       "l2": "inputs (>4 GB) exceed L2; also flushed between timed solves (256 MiB write)"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "per_step": parts},
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": profile_traffic(), "peak_source": peak_kind,
-                         "bytes_per_launch": by, "launch_us": 1e3 * ms},
+                    "steps": e2e_steps, "per_step": parts},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": dk["alg_gbs"], "peak": peak, "unit": "GB/s",
+                         "frac": dk["alg_gbs"] / peak, "traffic": traffic.get("dram_bytes_per_launch"),
+                         "peak_source": peak_kind, "bytes_per_launch": dk["alg_bytes"],
+                         "moved_bytes_per_launch": dk["moved_bytes"], "moved_frac": dk["moved_gbs"] / peak,
+                         "launch_us": dk["us"], "panels": dk["panels"],
+                         "traffic_source": traffic.get("source")},
             "iteration_roofline": {"b_iter_bytes": b_iter(n, m, nnz),
                                    "achieved_gbs": b_iter(n, m, nnz) * value / world / 1e9,
                                    "frac": b_iter(n, m, nnz) * value / world / 1e9 / peak},
-            "kernels_us": {"dual": 1e3 * dual_ms, "primal": 1e3 * prim_ms},
-            "spmv": spmv,
-            "solve_1e-8": tol8,
+            "kernels": kern,
             "time_to_tolerance_ms": 1e3 * last.info["device_seconds"], "iterations": last.iterations,
-            # with chained windows (the default graph engine) the evaluations run
-            # inside the window graphs: window_ms then includes them
             "window_ms": 1e3 * last.info["window_seconds"], "eval_ms": 1e3 * last.info["eval_seconds"],
             "windows_chained": last.info["eval_seconds"] == 0.0,
             "host_gap_ms": 1e3 * (last.info["device_seconds"] - last.info["window_seconds"]
                                   - last.info["eval_seconds"]),
             "restarts": last.restarts, "status": str(last.status),
             "primal_objective": last.info["primal_objective"],
-            "setup_ms": 1e3 * last.info["setup_seconds"],
-            "gpu_launches": int(launches), "clocks": clk,
-            "wall_s": wall,
+            "setup_ms": 1e3 * last.info["setup_seconds"], "create_s": setup_s, "generate_s": gen_s,
+            "gpu_launches": int(launches), "clocks": clk, "wall_s": wall,
         }
+        if c2:
+            line["c2"] = c2
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
@@ -354,10 +445,15 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-iters", type=int, default=CPU_SAMPLE_ITERS)
+    ap.add_argument("--cpu-iters", type=int, default=4, help="CPU baseline sample (iterations, 1 core)")
+    ap.add_argument("--ref-iters", type=int, default=1, help="reference arm: iterations per solve per step")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-c2", action="store_true")
+    ap.add_argument("--cpu-sample", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
-    if args.impl == "reference":
+    if args.cpu_sample:
+        cpu_sample_main(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -283,6 +283,13 @@ int pdlp_get_iterate(pdlp_handle* h, double* x, double* y, double* kx, double* k
  * algorithmic bytes one launch moves. */
 int pdlp_time_kernel(pdlp_handle* h, int32_t which, int32_t reps, double* avg_ms,
                      double* bytes_per_launch);
+/* Bytes of one launch of kernel `which` (0 dual, 1 primal, 2 SpMV K x, 3 SpMV
+ * K^T y): out[0] = SURVEY.md §8(d)'s algorithmic bytes (what pdlp_time_kernel
+ * reports), out[1] = the bytes the launched variant moves at one DRAM access
+ * per element (bounds skipped when all [0, +inf), K'y' not stored under lazy
+ * K'y, column panels' counts / block offsets / running sums), out[2] = the
+ * operator's column-panel count (0: one tiled pass). (new; bench roofline) */
+int pdlp_kernel_bytes(pdlp_handle* h, int32_t which, double* out);
 
 /* Problem sizes after create: {n, m, m1, nnz}. */
 int pdlp_get_sizes(pdlp_handle* h, int64_t* sizes);

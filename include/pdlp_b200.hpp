@@ -20,6 +20,7 @@
 // numerical trouble is a status (SolveStatus::kNumericalError).
 #pragma once
 
+#include <cmath>
 #include <cstdint>
 #include <limits>
 #include <optional>
@@ -76,6 +77,20 @@ struct CsrMatrix {
   std::vector<double> values;
 
   index_t nnz() const { return static_cast<index_t>(values.size()); }
+  /// Array sizes and offsets the C ABI reads through raw pointers (the
+  /// reference's vector-backed CsrMatrix cannot be malformed this way).
+  void validate_storage(const char* which) const {
+    const std::string w(which);
+    if (num_rows < 0 || num_cols < 0) throw std::invalid_argument(w + ": negative dimension");
+    if (row_offsets.size() != static_cast<std::size_t>(num_rows) + 1)
+      throw std::invalid_argument(w + ": row_offsets must have num_rows + 1 entries");
+    if (col_indices.size() != values.size())
+      throw std::invalid_argument(w + ": col_indices and values differ in length");
+    if (row_offsets.front() != 0 || row_offsets.back() != nnz())
+      throw std::invalid_argument(w + ": row_offsets must run from 0 to nnz");
+    for (std::size_t r = 0; r + 1 < row_offsets.size(); ++r)
+      if (row_offsets[r + 1] < row_offsets[r]) throw std::invalid_argument(w + ": row_offsets not monotone");
+  }
   static CsrMatrix zero(index_t rows, index_t cols) {
     CsrMatrix m;
     m.num_rows = rows;
@@ -100,6 +115,31 @@ struct GeneralFormLp {
   index_t num_inequalities() const { return inequality_matrix.num_rows; }
   index_t num_equalities() const { return equality_matrix.num_rows; }
   index_t num_constraints() const { return num_inequalities() + num_equalities(); }
+
+  /// GeneralFormLp::validate (lp_model.hpp:45-72), same checks and messages,
+  /// plus the CSR storage checks the raw-pointer ABI needs.
+  void validate() const {
+    inequality_matrix.validate_storage("lp: inequality matrix");
+    equality_matrix.validate_storage("lp: equality matrix");
+    const index_t n = num_variables();
+    if (inequality_matrix.num_cols != n || equality_matrix.num_cols != n)
+      throw std::invalid_argument("lp: constraint matrices must have n columns");
+    if (static_cast<index_t>(inequality_rhs.size()) != num_inequalities() ||
+        static_cast<index_t>(equality_rhs.size()) != num_equalities())
+      throw std::invalid_argument("lp: rhs length does not match row count");
+    if (static_cast<index_t>(lower.size()) != n || static_cast<index_t>(upper.size()) != n)
+      throw std::invalid_argument("lp: bound vectors must have length n");
+    const double inf = std::numeric_limits<double>::infinity();
+    for (index_t i = 0; i < n; ++i) {
+      const double l = lower[static_cast<std::size_t>(i)], u = upper[static_cast<std::size_t>(i)];
+      if (std::isnan(l) || std::isnan(u))
+        throw std::invalid_argument("lp: NaN bound on variable " + std::to_string(i));
+      if (l > u || l == inf || u == -inf)
+        throw std::invalid_argument("lp: empty bound interval on variable " + std::to_string(i));
+    }
+    for (double v : objective)
+      if (std::isnan(v)) throw std::invalid_argument("lp: NaN objective entry");
+  }
 };
 
 struct SolverParams {
@@ -275,6 +315,7 @@ inline std::vector<index_t> widen(const int64_t* p, int64_t n) { return {p, p + 
 class Solver {
  public:
   Solver(const GeneralFormLp& lp, const SolverParams& params = {}) {
+    lp.validate();
     params.validate();
     const pdlp_lp v = detail::view(lp);
     const pdlp_params p = detail::to_c(params);

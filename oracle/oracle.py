@@ -132,6 +132,21 @@ class Session:
         self.status = st.value
         return st.value
 
+    def fork(self) -> "Session":
+        """An independent copy of the iterate state sharing the read-only setup
+        (reference harness only)."""
+        if self.kind != "ref":
+            raise ValueError("fork: reference sessions only")
+        fn = self.lib.ref_fork
+        fn.restype, fn.argtypes = C.c_void_p, [C.c_void_p]
+        s = Session.__new__(Session)
+        s.kind, s.lib, s.params, s._lp, s.n, s.m, s.status = self.kind, self.lib, self.params, self._lp, \
+            self.n, self.m, self.status
+        s.h = fn(self.h)
+        if not s.h:
+            raise RuntimeError(_f(self.lib, self.kind, "last_error")().decode())
+        return s
+
     def iterate(self) -> dict:
         x, y, kx, kty = np.zeros(self.n), np.zeros(self.m), np.zeros(self.m), np.zeros(self.n)
         cnt, sc = np.zeros(4, np.int64), np.zeros(4)

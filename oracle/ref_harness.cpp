@@ -24,6 +24,7 @@
 #include <cstdio>
 #include <cstring>
 #include <exception>
+#include <memory>
 #include <optional>
 #include <string>
 #include <vector>
@@ -159,13 +160,30 @@ void copy_logs(const SolveResult& r, pdlp_step_log_entry* sl, int64_t scap,
 // Re-driven SolveLoop::run (solver.hpp:759-929) using the reference's own
 // building blocks, paused every `count` accepted iterations so per-iterate
 // state can be read. SolveLoop keeps these members private, hence the mirror.
-struct Session {
+// The read-only part (the instance, its scaling and saddle form) is shared by
+// forked sessions (ref_fork): concurrent independent solves of one instance
+// without one copy of the operators per thread.
+struct Setup {
   GeneralFormLp lp;
   SolverParams p;
   TerminationNorms norms;
   DiagonalScaling scaling;
   GeneralFormLp scaled;
   SaddleProblem saddle;
+};
+
+struct Session {
+  explicit Session(std::shared_ptr<Setup> s)
+      : su(std::move(s)), lp(su->lp), p(su->p), norms(su->norms), scaling(su->scaling),
+        scaled(su->scaled), saddle(su->saddle) {}
+  Session(const Session&) = default;
+  std::shared_ptr<Setup> su;
+  const GeneralFormLp& lp;
+  const SolverParams& p;
+  const TerminationNorms& norms;
+  const DiagonalScaling& scaling;
+  const GeneralFormLp& scaled;
+  const SaddleProblem& saddle;
   PrimalDualPoint current, epoch_start, last_delta;
   std::vector<double> kx, kty;
   WeightedAverage avg_x{0}, avg_y{0};
@@ -222,12 +240,15 @@ struct Session {
     finished = true;
   }
 
+  static void prepare(Setup& su) {
+    su.norms = termination_norms(su.lp);
+    su.scaling = make_scaling(vstack(su.lp.inequality_matrix, su.lp.equality_matrix), su.p.scaling,
+                              su.p.ruiz_iterations, su.p.pock_chambolle_alpha);
+    su.scaled = apply_scaling(su.lp, su.scaling);
+    su.saddle = to_saddle(su.scaled);
+  }
+
   void begin() {
-    norms = termination_norms(lp);
-    scaling = make_scaling(vstack(lp.inequality_matrix, lp.equality_matrix), p.scaling,
-                           p.ruiz_iterations, p.pock_chambolle_alpha);
-    scaled = apply_scaling(lp, scaling);
-    saddle = to_saddle(scaled);
     t0 = std::chrono::steady_clock::now();
     const index_t n = saddle.num_variables(), m = saddle.num_constraints();
     current = PrimalDualPoint::zeros(n, m);
@@ -387,11 +408,13 @@ int ref_solve(const pdlp_lp* lp, const pdlp_params* params, pdlp_result_info* in
 
 void* ref_begin(const pdlp_lp* lp, const pdlp_params* params, int32_t* status) {
   try {
-    auto* s = new Session;
-    s->lp = to_lp(*lp);
-    s->lp.validate();
-    s->p = to_params(*params);
-    s->p.validate();
+    auto su = std::make_shared<Setup>();
+    su->lp = to_lp(*lp);
+    su->lp.validate();
+    su->p = to_params(*params);
+    su->p.validate();
+    Session::prepare(*su);
+    auto* s = new Session(std::move(su));
     s->begin();
     if (status) *status = s->finished ? static_cast<int32_t>(s->result.status) : PDLP_STATUS_RUNNING;
     return s;
@@ -447,6 +470,17 @@ int ref_result(void* h, pdlp_result_info* info, double* x, double* y, double* la
 }
 
 void ref_end(void* h) { delete static_cast<Session*>(h); }
+
+// An independent copy of a session's iterate state sharing its read-only
+// setup (bench.py's reference arm: one concurrent solve per host core).
+void* ref_fork(void* h) {
+  try {
+    return new Session(*static_cast<const Session*>(h));
+  } catch (const std::exception& e) {
+    fail(PDLP_ERUNTIME, e.what());
+    return nullptr;
+  }
+}
 
 int ref_scaling(const pdlp_lp* lp, const pdlp_params* params, double* row_scale, double* col_scale) {
   try {

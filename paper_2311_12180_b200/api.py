@@ -60,6 +60,7 @@ def load_library(build_if_missing: bool = True) -> C.CDLL:
         "pdlp_iterate_run": (C.c_int, [H, C.c_int64, i32p]),
         "pdlp_get_iterate": (C.c_int, [H, dp, dp, dp, dp, i64p, dp]),
         "pdlp_time_kernel": (C.c_int, [H, C.c_int32, C.c_int32, dp, dp]),
+        "pdlp_kernel_bytes": (C.c_int, [H, C.c_int32, dp]),
         "pdlp_get_sizes": (C.c_int, [H, i64p]),
         "pdlp_last_error": (C.c_char_p, []),
         "pdlp_read_mps": (C.c_int, [C.c_char_p, C.c_int32, C.POINTER(H)]),
@@ -111,6 +112,7 @@ class Solver:
     def __init__(self, lp: GeneralFormLp, params: SolverParams | None = None):
         self._lib = load_library()
         self.params = params or SolverParams()
+        lp.validate()  # the C ABI reads the arrays through raw pointers
         self._lp = lp  # keeps the host arrays alive during create
         self._h = C.c_void_p()
         lpa = lp.to_abi()
@@ -162,7 +164,10 @@ class Solver:
     # ---- kernel-level entry points ----
     def spmv(self, op: int, v: np.ndarray) -> np.ndarray:
         v = np.ascontiguousarray(v, dtype=np.float64)
-        out = np.zeros(self.n if op in (abi.OP_KT_SCALED, abi.OP_KT_ORIGINAL) else self.m)
+        transpose = op in (abi.OP_KT_SCALED, abi.OP_KT_ORIGINAL)
+        if v.ndim != 1 or v.size != (self.m if transpose else self.n):
+            raise ValueError("spmv: dimension mismatch")  # sparse_matrix.hpp:119-122,144-147
+        out = np.zeros(self.n if transpose else self.m)
         _check(self._lib.pdlp_spmv(self._h, op, abi.dptr(v), abi.dptr(out)))
         return out
 
@@ -217,6 +222,13 @@ class Solver:
         ms, by = C.c_double(), C.c_double()
         _check(self._lib.pdlp_time_kernel(self._h, which, reps, C.byref(ms), C.byref(by)))
         return ms.value, by.value
+
+    def kernel_bytes(self, which: int) -> dict:
+        """Algorithmic and moved bytes of one launch of kernel
+        `which` (0 dual, 1 primal, 2 K x, 3 K^T y), and the panel count."""
+        out = (C.c_double * 3)()
+        _check(self._lib.pdlp_kernel_bytes(self._h, which, out))
+        return {"algorithmic": out[0], "moved": out[1], "panels": int(out[2])}
 
 
 def csr_from_triplets(rows: int, cols: int, r, c, v, device: int = 0):

@@ -177,6 +177,15 @@ int pdlp_time_kernel(pdlp_handle* h, int32_t which, int32_t reps, double* avg_ms
   return guarded([&] { h->solver->time_kernel(which, reps, avg_ms, bytes_per_launch); });
 }
 
+int pdlp_kernel_bytes(pdlp_handle* h, int32_t which, double* out) {
+  if (!h) return null_handle();
+  return guarded([&] {
+    if (!out || which < 0 || which > 3) throw std::invalid_argument("pdlp_kernel_bytes: which must be 0..3");
+    h->solver->kernel_bytes(which, out, out + 1);
+    out[2] = double(h->solver->panels(which == 0 || which == 2 ? 0 : 1));
+  });
+}
+
 int pdlp_get_sizes(pdlp_handle* h, int64_t* sizes) {
   if (!h) return null_handle();
   return guarded([&] { h->solver->sizes(sizes); });
@@ -219,6 +228,8 @@ int pdlp_shard_import(pdlp_handle* h, const void* blobs, int32_t world) {
     return PDLP_EINVAL;
   }
   return guarded([&] {
+    if (world < 1 || world > pdlp::kMaxShards)
+      throw std::invalid_argument("shards: world must lie in [1, " + std::to_string(pdlp::kMaxShards) + "]");
     std::vector<pdlp::ShardBlob> v(static_cast<size_t>(world));
     std::memcpy(v.data(), blobs, sizeof(pdlp::ShardBlob) * size_t(world));
     h->solver->import_shards(v.data(), world);
@@ -240,6 +251,9 @@ int pdlp_plan_shards(const pdlp_lp* lp, int32_t world, int64_t* k_cuts, int64_t*
     return PDLP_EINVAL;
   }
   return guarded([&] {
+    if (world < 1 || world > pdlp::kMaxShards)
+      throw std::invalid_argument("shards: world must lie in [1, " + std::to_string(pdlp::kMaxShards) + "]");
+    pdlp::validate_lp(*lp);
     // row offsets of K = vstack(G, A) and of K^T (column counts), on the host
     const pdlp_csr& G = lp->inequality_matrix;
     const pdlp_csr& A = lp->equality_matrix;

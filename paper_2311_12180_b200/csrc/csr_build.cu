@@ -12,6 +12,7 @@
 // values are bit-exact wherever a (row, col) pair occurs at most twice (the
 // reference's per-row std::sort is unstable, so the summation order of three
 // or more duplicates is unspecified there).
+#include <limits>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -96,6 +97,10 @@ void csr_from_triplets(int64_t rows, int64_t cols, int64_t nt, const int64_t* hr
                        const double* hv, int64_t* row_offsets, int64_t* col_indices, double* values,
                        int64_t* nnz_out) {
   if (rows < 0 || cols < 0 || nt < 0) throw std::invalid_argument("from_triplets: negative dimension");
+  // the sort key is row * cols + col in 63 bits: distinct (row, col) pairs must
+  // not alias (the reference's per-row sort has no such limit)
+  if (cols > 0 && rows > std::numeric_limits<int64_t>::max() / cols)
+    throw std::invalid_argument("from_triplets: rows * cols exceeds the 63-bit key range");
   cudaStream_t s;
   PDLP_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   struct StreamGuard {

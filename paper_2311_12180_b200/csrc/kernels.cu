@@ -1315,6 +1315,7 @@ void set_kernel_attributes() {
   big((const void*)eval_rows_kernel<true>, stream_smem_bytes<Ev1Epi<true>>());
   big((const void*)eval_cols_kernel<false>, stream_smem_bytes<Ev2Epi<false>>());
   big((const void*)eval_cols_kernel<true>, stream_smem_bytes<Ev2Epi<true>>());
+  panel_kernel_attributes();
 }
 
 void launch_build_rowptr(const int64_t* g_off, const int64_t* a_off, int64_t m1, int64_t m2,

@@ -92,16 +92,30 @@ void launch_reduced_of_objective(const double* c, const double* l, const double*
                                  double* lam, cudaStream_t s);
 
 // ---- column panels (panels.cu) ---------------------------------------------
+// Device view of one panelized operator (panel-major entries, per-panel row
+// counts and block offsets, running row sums between passes).
+struct PanelView {
+  const int* col;
+  const double* val;
+  const unsigned char* cnt;  // [panels][rows_pad] entries of each row in each panel
+  const int* boff;           // [panels][nblk + 1] first entry of each 1024-row block
+  double* acc;               // [rows] running row sums between passes
+  int rows, rows_pad, nblk, panels;
+};
 void launch_panel_keys(const int* row_of, const int* col, int64_t nnz, int width, int rows, int* keys,
                        cudaStream_t s);
 void launch_panel_gather(const int* perm, const int* col, const double* val, int64_t nnz, int* col_p,
                          double* val_p, cudaStream_t s);
 void launch_panel_spread(const int* rp, const int* col, int rows, int width, unsigned long long* distinct,
                          cudaStream_t s);
-int panel_combine_blocks(int rows);
-void launch_panel_dual(const DevCsr& kp, int panels, double* partial, const DevIter& it, cudaStream_t s);
-void launch_panel_primal(const DevCsr& ktp, int panels, double* partial, const DevIter& it, int mode_override,
-                         cudaStream_t s);
+void launch_panel_meta(const int* counts, const int* so, int rows, int rows_pad, int panels, int nblk,
+                       unsigned char* cnt, int* boff, int* over, cudaStream_t s);
+int panel_rows_pad(int rows);
+int panel_blocks(int rows);  // 1024-row blocks = CTAs per pass = reduction partials of the last pass
+void launch_panel_dual(const PanelView& kp, const DevIter& it, cudaStream_t s);
+void launch_panel_primal(const PanelView& ktp, const DevIter& it, int mode_override, cudaStream_t s);
+void launch_panel_spmv(const PanelView& pv, const double* v, double* out, cudaStream_t s);
+void panel_kernel_attributes();  // dynamic shared memory of the sweep kernels (once per device)
 
 void set_kernel_attributes();
 

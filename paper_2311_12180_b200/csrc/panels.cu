@@ -1,18 +1,32 @@
-// panels.cu — column-panel SpMV for operators whose gathered vector is much
+// panels.cu — column-panel sweeps for operators whose gathered vector is far
 // larger than L2 and whose rows scatter over it (C4: random columns over a
-// 320 MB x; ncu shows ~100 B of DRAM traffic per gathered element, 6x the
-// algorithmic bytes, because every miss fetches a line for one double).
+// 320 MB x and a 160 MB y; a direct gather pulls a 32-byte DRAM sector per
+// nonzero). Reference: spmv (sparse_matrix.hpp:117-132) and spmv_transpose
+// (:142-158, as a gather over the stored K^T), inside adaptive_step_cached
+// (solver.hpp:409,456).
 //
-// The operator's entries are re-ordered panel-major: panel p holds the entries
-// whose column lies in [p w, (p+1) w), stored as a CSR of P * rows "stacked"
-// rows (p, r). One pass of the ordinary tiled SpMV over the stacked CSR, in
-// tile order, walks the panels one after another, so the running CTAs gather
-// from one L2-sized slice of the vector at a time; it writes one partial sum
-// per (panel, row). A combine kernel then adds each row's P partials in panel
-// order and applies the fused update of the dual or primal kernel (the same
-// epilogue code, DualEpi / PrimalEpi) with its reductions.
+// Layout. The entries are re-ordered panel-major: panel p holds the entries
+// whose column lies in [p w, (p+1) w), row by row, each row's entries in
+// column order. Per panel, a byte per row gives the row's entry count in that
+// panel (`cnt`), and one int per warp block of 128 rows gives the block's
+// first entry (`boff`); no per-(panel, row) offsets are stored.
 //
-// Fast mode on one device only (the per-row sum order changes: panels first).
+// Iteration. Pass p (one launch per panel) walks every block of 1024 rows
+// (one CTA, 4 rows per thread). Every load a CTA needs is issued up front and
+// only the true dependences wait: the block's first entry (`boff`, L2) ->
+// its indices (HBM) -> the gathers of v[col] (the L2-resident panel slice),
+// with the values, the count bytes and the running sums arriving meanwhile;
+// the products are staged in shared memory and each thread continues its
+// rows' running sums over them in entry order. The running sums live in `acc`
+// between passes (16 B per row per pass); the last pass applies the fused
+// update of the dual or primal kernel (DualEpi / PrimalEpi) instead, with one
+// reduction partial per block. (TMA bulk copies of the blocks, per CTA with a
+// 2-3 stage ring and per warp, were measured 1.7-2.3x slower on C4.)
+//
+// Every row is summed by one thread, starting from 0.0, in increasing column
+// order: exactly the reference's `out[r] += val * x[col]` sequence. The panel
+// sweep is therefore bitwise equal to the sequential SpMV (and to the tiled
+// engine's STREAM rows), whatever the panel count.
 #include "epilogues.cuh"
 #include "kernels.cuh"
 #include "spmv_engine.cuh"
@@ -27,21 +41,54 @@ int grid_n(int64_t n) {
   return int(g);
 }
 
-struct PartialEpi : EpiBase<PartialEpi> {
-  static constexpr int NP = 1, NA = 1, NR = 1;
-  static constexpr bool kEvictFirst = true;  // the stacked operator streams through L2 once per pass
-  // (no kUniform: stacked rows are short and irregular)
-  static constexpr TileGeom kGeom = kPanelGeom;
-  static constexpr bool kNeedCol = false;
-  const double* __restrict__ x;
-  double* __restrict__ out;
-  __device__ __forceinline__ void gather(int c, double (&g)[1]) const { g[0] = __ldg(x + c); }
-  __device__ __forceinline__ void add(double (&a)[1], const double (&p)[1], int) const { a[0] += p[0]; }
-  __device__ __forceinline__ void row_done(int r, const double (&a)[1], double (&)[1]) const { out[r] = a[0]; }
-};
+__device__ __forceinline__ unsigned ld_stream_u32_ef(const unsigned char* p, uint64_t pol) {
+  unsigned r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ int ld_stream_i1_ef(const int* p, uint64_t pol) {
+  int r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ double ld_stream_d1_ef(const double* p, uint64_t pol) {
+  double r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ double ld_acc(const double* p) {
+  double r;
+  asm volatile("ld.global.cs.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_acc(double* p, double v) {
+  asm volatile("st.global.cs.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
 }  // namespace
 
-// ---- setup: stacked panel CSR ---------------------------------------------
+using SweepOp = PanelView;
+
+constexpr int kSweepRows = kIterGeom.stream_rows;  // rows per CTA: 4 per thread, stride kThreads
+constexpr int kSweepRPT = kSweepRows / kThreads;
+#ifndef PDLP_SWEEP_CHUNK
+#define PDLP_SWEEP_CHUNK 2048
+#endif
+#ifndef PDLP_SWEEP_CTAS
+#define PDLP_SWEEP_CTAS 4
+#endif
+constexpr int kSweepChunk = PDLP_SWEEP_CHUNK;      // products staged per round (16 KB)
+constexpr int kSweepPer = kSweepChunk / kThreads;  // entries per thread per round, all in flight
+constexpr int kSweepCtasPerSm = PDLP_SWEEP_CTAS;
+static_assert(kSweepRows == 4 * kThreads, "four count bytes and four rows per thread");
+
+struct SweepSmem {
+  int off[kSweepRows + 1];
+  int warp[kWarps + 1];
+  double prod[kSweepChunk];
+};
+
+// ---- setup -----------------------------------------------------------------
 
 __global__ void panel_keys_kernel(const int* row_of, const int* col, int64_t nnz, int width, int rows,
                                   int* keys) {
@@ -73,6 +120,26 @@ __global__ void panel_spread_kernel(const int* rp, const int* col, int rows, int
   atomicAdd(distinct, local);  // integer: order-free
 }
 
+// cnt[p][r] (bytes) and boff[p][b] from the per-(panel, row) counts and their
+// exclusive scan `so` over the stacked rows (p, r); `over` flags a count > 255.
+__global__ void panel_meta_kernel(const int* counts, const int* so, int rows, int rows_pad, int panels, int nblk,
+                                  unsigned char* cnt, int* boff, int* over) {
+  const int64_t total = int64_t(panels) * rows_pad;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int p = int(i / rows_pad), r = int(i % rows_pad);
+    int cv = 0;
+    if (r < rows) cv = counts[int64_t(p) * rows + r];
+    if (cv > 255) atomicOr(over, 1);
+    cnt[i] = (unsigned char)(cv > 255 ? 255 : cv);
+  }
+  const int64_t nb = int64_t(panels) * (nblk + 1);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nb; i += int64_t(gridDim.x) * blockDim.x) {
+    const int p = int(i / (nblk + 1)), b = int(i % (nblk + 1));
+    const int64_t r = int64_t(b) * kSweepRows < rows ? int64_t(b) * kSweepRows : int64_t(rows);
+    boff[i] = so[int64_t(p) * rows + r];
+  }
+}
+
 void launch_panel_keys(const int* row_of, const int* col, int64_t nnz, int width, int rows, int* keys,
                        cudaStream_t s) {
   panel_keys_kernel<<<grid_n(nnz), kThreads, 0, s>>>(row_of, col, nnz, width, rows, keys);
@@ -88,18 +155,130 @@ void launch_panel_spread(const int* rp, const int* col, int rows, int width, uns
   panel_spread_kernel<<<grid_n(rows), kThreads, 0, s>>>(rp, col, rows, width, distinct);
   PDLP_CUDA(cudaGetLastError());
 }
+void launch_panel_meta(const int* counts, const int* so, int rows, int rows_pad, int panels, int nblk,
+                       unsigned char* cnt, int* boff, int* over, cudaStream_t s) {
+  panel_meta_kernel<<<grid_n(int64_t(panels) * rows_pad), kThreads, 0, s>>>(counts, so, rows, rows_pad, panels,
+                                                                            nblk, cnt, boff, over);
+  PDLP_CUDA(cudaGetLastError());
+}
+int panel_rows_pad(int rows) { return (rows + kSweepRows - 1) / kSweepRows * kSweepRows; }
+int panel_blocks(int rows) { return (rows + kSweepRows - 1) / kSweepRows; }
 
-// ---- iteration ------------------------------------------------------------
+// ---- iteration ---------------------------------------------------------------
 
-// Pass 1: partial[p * rows + r] = sum over panel p of row r. The dual gathers
-// x' (the trial primal); the primal gathers the current y after the decision
-// (decide_kernel committed it) and skips when the branch needs no K'y.
+namespace {
+
+// Exclusive block scan of one int per thread (fixed order; integers).
+__device__ __forceinline__ int block_excl_scan(int v, int* s_warp /* kWarps + 1 */, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int t = lane < kWarps ? s_warp[lane] : 0;
+    int ti = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, ti, o);
+      if (lane >= o) ti += u;
+    }
+    if (lane < kWarps) s_warp[lane] = ti - t;
+    if (lane == kWarps - 1) s_warp[kWarps] = ti;
+  }
+  __syncthreads();
+  *total = s_warp[kWarps];
+  return s_warp[warp] + incl - v;
+}
+
+// Continues the running sums acc[i] of this thread's rows b R + tid + i kThreads
+// over panel p of v (acc[] = 0.0 at p = 0, else the sums loaded from `acc`);
+// returns a bit per row with entries in this panel.
+__device__ __forceinline__ unsigned sweep_block(const SweepOp& op, int p, int b, const double* __restrict__ v,
+                                                double (&acc)[kSweepRPT], SweepSmem& sm) {
+  const int tid = threadIdx.x;
+  const uint64_t ef = l2_evict_first_policy();
+  // independent loads first: the block's entry range, its count bytes, the sums
+  const int* bo = op.boff + size_t(p) * (op.nblk + 1) + b;
+  const int e0 = __ldg(bo), e1 = __ldg(bo + 1);
+  const unsigned cw = ld_stream_u32_ef(op.cnt + size_t(p) * op.rows_pad + size_t(b) * kSweepRows + 4 * tid, ef);
+  const int r0 = b * kSweepRows + tid;
+#pragma unroll
+  for (int q = 0; q < kSweepRPT; ++q) acc[q] = p > 0 ? ld_acc(op.acc + r0 + q * kThreads) : 0.0;
+  const int E = e1 - e0;
+  const int* __restrict__ col = op.col + e0;
+  const double* __restrict__ val = op.val + e0;
+  // the first round's products need only the entry range: staged before the scan
+  auto stage = [&](int c0, int c1) {
+    int cc[kSweepPer];
+#pragma unroll
+    for (int j = 0; j < kSweepPer; ++j) {
+      const int k = c0 + tid + j * kThreads;
+      cc[j] = k < c1 ? ld_stream_i1_ef(col + k, ef) : 0;
+    }
+    double g[kSweepPer];
+#pragma unroll
+    for (int j = 0; j < kSweepPer; ++j) {
+      const int k = c0 + tid + j * kThreads;
+      if (k < c1) g[j] = __ldg(v + cc[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < kSweepPer; ++j) {
+      const int k = c0 + tid + j * kThreads;
+      if (k < c1) sm.prod[k - c0] = ld_stream_d1_ef(val + k, ef) * g[j];  // rounded product, as val * x
+    }
+  };
+  stage(0, min(E, kSweepChunk));
+  // row offsets inside the block (4 rows' count bytes per thread, block scan)
+  int c[4], tot = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) c[i] = int((cw >> (8 * i)) & 255u), tot += c[i];
+  int Et;
+  const int ex = block_excl_scan(tot, sm.warp, &Et);  // (its barriers also publish the staged products)
+  sm.off[4 * tid] = ex;
+  sm.off[4 * tid + 1] = ex + c[0];
+  sm.off[4 * tid + 2] = ex + c[0] + c[1];
+  sm.off[4 * tid + 3] = ex + c[0] + c[1] + c[2];
+  if (tid == kThreads - 1) sm.off[kSweepRows] = Et;
+  __syncthreads();
+  int o[kSweepRPT], e[kSweepRPT];
+  unsigned has = 0;
+#pragma unroll
+  for (int q = 0; q < kSweepRPT; ++q) {
+    const int r = tid + q * kThreads;
+    o[q] = sm.off[r];
+    e[q] = sm.off[r + 1];
+    has |= (e[q] > o[q] ? 1u : 0u) << q;
+  }
+  for (int c0 = 0; c0 < E; c0 += kSweepChunk) {
+    const int c1 = min(E, c0 + kSweepChunk);
+    if (c0 > 0) {  // a further round of an oversized block
+      __syncthreads();
+      stage(c0, c1);
+      __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < kSweepRPT; ++q) {
+      const int k0 = max(o[q], c0), k1 = min(e[q], c1);
+      for (int k = k0; k < k1; ++k) acc[q] = acc[q] + sm.prod[k - c0];  // sparse_matrix.hpp:128-130
+    }
+  }
+  return has;
+}
+
+}  // namespace
+
+// Passes 0 .. P-2: the dual gathers x' (the trial primal); the primal gathers
+// the current y after the decision (decide_kernel committed it) and skips when
+// the branch needs no K'y.
 template <bool kPrimal>
-__global__ void __launch_bounds__(kThreads, 4) panel_spmv_kernel(DevCsr A, DevIter it, double* partial,
-                                                                 int mode_override) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const Tile t = A.tiles[blockIdx.x];
-  if (it.prefetch) prefetch_tile(t, A.rp, A.col, A.val);
+__global__ void __launch_bounds__(kThreads, kSweepCtasPerSm) sweep_pass_kernel(SweepOp op, DevIter it, int p,
+                                                                             int mode_override) {
+  __shared__ SweepSmem sm;
   griddep_wait();
   const DevState* st = it.st;
   const double* src;
@@ -112,19 +291,23 @@ __global__ void __launch_bounds__(kThreads, 4) panel_spmv_kernel(DevCsr A, DevIt
     if (!(mode == kPAccept || mode == kPRestart || lazy_retry)) return;
     src = it.y[st->iy_cur];
   }
-  PartialEpi epi;
-  epi.x = src;
-  epi.out = partial;
-  double red[1] = {0.0};
-  run_tile<PartialEpi, false>(t, A.rp, A.col, A.val, epi, red, A.chunk_part, A.chunk_ctr, smem);
+  const int b = blockIdx.x;
+  double acc[kSweepRPT];
+  const unsigned has = sweep_block(op, p, b, src, acc, sm);
   griddep_launch_dependents();
+  const int r0 = b * kSweepRows + threadIdx.x;
+#pragma unroll
+  for (int q = 0; q < kSweepRPT; ++q) {
+    const int r = r0 + q * kThreads;
+    if (r < op.rows && (p == 0 || ((has >> q) & 1u))) st_acc(op.acc + r, acc[q]);
+  }
 }
 
-// Pass 2 of the dual: CTA 0 is the helper (state snapshot, dx^2 of x'); CTA
-// b >= 1 combines rows [(b-1) R, b R), R = kIterGeom.stream_rows, and applies
-// the dual update (DualEpi) with its partials at slot b-1.
-__global__ void __launch_bounds__(kThreads, 4) dual_combine_kernel(DevIter it, const double* partial,
-                                                                   int panels) {
+// Last pass of the dual: CTA 0 is the helper (state snapshot, dx^2 of x'); CTA
+// b >= 1 finishes rows [(b-1) R, b R) and applies the dual update (DualEpi)
+// with its partials at slot b-1.
+__global__ void __launch_bounds__(kThreads, kSweepCtasPerSm) sweep_dual_final_kernel(SweepOp op, DevIter it) {
+  __shared__ SweepSmem sm;
   griddep_wait();
   DevState* st = it.st;
   const bool parked = st->failure || st->window_accepts >= st->window_target;
@@ -139,9 +322,14 @@ __global__ void __launch_bounds__(kThreads, 4) dual_combine_kernel(DevIter it, c
     return;
   }
   if (parked) return;
-  constexpr int RPT = kIterGeom.stream_rows / kThreads;
   const int b = blockIdx.x - 1;
-  const int r0 = b * kIterGeom.stream_rows + threadIdx.x;
+  const int r0 = b * kSweepRows + threadIdx.x;
+  double acc[kSweepRPT];
+  sweep_block(op, op.panels - 1, b, it.x[st->ix_trial], acc, sm);
+  int nvalid = 0;
+#pragma unroll
+  for (int q = 0; q < kSweepRPT; ++q)
+    if (r0 + q * kThreads < op.rows) nvalid = q + 1;
   DualEpi<false> epi;
   epi.xg = nullptr;
   epi.y = it.y[st->iy_cur];
@@ -151,31 +339,23 @@ __global__ void __launch_bounds__(kThreads, 4) dual_combine_kernel(DevIter it, c
   epi.kxt = it.kx[1 - st->ikx_cur];
   epi.sigma = st->eta * st->omega;  // sigma = eta * omega, solver.hpp:402
   epi.m1 = it.m1;
-  double acc[RPT][1];
-  int nvalid = 0;
+  double a2[kSweepRPT][1];
 #pragma unroll
-  for (int i = 0; i < RPT; ++i) {
-    const int r = r0 + i * kThreads;
-    acc[i][0] = 0.0;
-    if (r < it.m) {
-      nvalid = i + 1;
-      for (int p = 0; p < panels; ++p) acc[i][0] += __ldcg(partial + size_t(p) * it.m + r);
-    }
-  }
+  for (int q = 0; q < kSweepRPT; ++q) a2[q][0] = acc[q];
   double red[3] = {0.0, 0.0, 0.0};
-  epi.rows_strided<RPT>(r0, kThreads, nvalid, acc, red);
+  epi.rows_strided<kSweepRPT>(r0, kThreads, nvalid, a2, red);
   griddep_launch_dependents();
   store_partial<3, 0>(red, it.d_part, b, it.d_tiles);
 }
 
-// Pass 2 of the primal (decision already committed by decide_kernel): CTAs
-// b < nblk combine columns [b R, (b+1) R) and apply PrimalEpi (accept: with the
+// Last pass of the primal (decision already committed by decide_kernel): CTAs
+// b < nblk finish columns [b R, (b+1) R) and apply PrimalEpi (accept: with the
 // averages; restart / lazy retry: without), or recompute x' from the kept K'y
 // (retry); the trailing CTAs update avg_y on accepted steps.
 template <bool kNonneg>
-__global__ void __launch_bounds__(kThreads, 4) primal_combine_kernel(DevIter it, const double* partial,
-                                                                     int panels, int nblk,
-                                                                     int mode_override) {
+__global__ void __launch_bounds__(kThreads, kSweepCtasPerSm) sweep_primal_final_kernel(SweepOp op, DevIter it,
+                                                                                     int mode_override) {
+  __shared__ SweepSmem sm;
   griddep_wait();
   DevState* st = it.st;
   const DevState& s = *st;
@@ -183,6 +363,7 @@ __global__ void __launch_bounds__(kThreads, 4) primal_combine_kernel(DevIter it,
   if (mode == kPNone) return;
   const double tau = s.eta / s.omega;  // tau = eta / omega, solver.hpp:401
   const int bid = blockIdx.x;
+  const int nblk = op.nblk;
   if (bid >= nblk) {  // avg_y .add (solver.hpp:839)
     if (mode == kPAccept) {
       const int nb = gridDim.x - nblk, b = bid - nblk;
@@ -194,11 +375,16 @@ __global__ void __launch_bounds__(kThreads, 4) primal_combine_kernel(DevIter it,
     }
     return;
   }
-  constexpr int RPT = kIterGeom.stream_rows / kThreads;
-  const int j0 = bid * kIterGeom.stream_rows + threadIdx.x;
+  const int j0 = bid * kSweepRows + threadIdx.x;
   const bool lazy_retry = it.kty_lazy && mode == kPRetry && mode_override < 0;
   double red[2] = {0.0, 0.0};
   if (mode == kPAccept || mode == kPRestart || lazy_retry) {
+    double acc[kSweepRPT];
+    sweep_block(op, op.panels - 1, bid, it.y[s.iy_cur], acc, sm);
+    int nvalid = 0;
+#pragma unroll
+    for (int q = 0; q < kSweepRPT; ++q)
+      if (j0 + q * kThreads < op.rows) nvalid = q + 1;
     const bool acc_step = mode == kPAccept;
     PrimalEpi<false, kNonneg> epi;
     epi.yg = nullptr;
@@ -215,25 +401,17 @@ __global__ void __launch_bounds__(kThreads, 4) primal_combine_kernel(DevIter it,
     epi.do_avg = acc_step;
     epi.avg_first = s.avg_first;
     epi.store_kty = (acc_step && it.kty_lazy) ? 0 : 1;
-    double acc[RPT][1];
-    int nvalid = 0;
+    double a2[kSweepRPT][1];
 #pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-      const int j = j0 + i * kThreads;
-      acc[i][0] = 0.0;
-      if (j < it.n) {
-        nvalid = i + 1;
-        for (int p = 0; p < panels; ++p) acc[i][0] += __ldcg(partial + size_t(p) * it.n + j);
-      }
-    }
-    epi.rows_strided<RPT>(j0, kThreads, nvalid, acc, red);
+    for (int q = 0; q < kSweepRPT; ++q) a2[q][0] = acc[q];
+    epi.template rows_strided<kSweepRPT>(j0, kThreads, nvalid, a2, red);
   } else if (mode == kPRetry) {
     const double* xc = it.x[s.ix_cur];
     const double* kty = it.kty[s.ikty_cur];
     double* xt = it.x[s.ix_trial];
 #pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-      const int j = j0 + i * kThreads;
+    for (int q = 0; q < kSweepRPT; ++q) {
+      const int j = j0 + q * kThreads;
       if (j < it.n) {
         const double xa = xc[j];
         const double v = xa - tau * (it.c[j] - kty[j]);
@@ -248,6 +426,29 @@ __global__ void __launch_bounds__(kThreads, 4) primal_combine_kernel(DevIter it,
   const size_t half = size_t(s.trials_total & 1) * it.p_tiles * 2;
   store_partial<2, 0>(red, it.p_part + half, bid, it.p_tiles);
 }
+
+// Plain SpMV through the panel sweep (bench / kernel parity): out = A v, the
+// last pass storing the sums.
+__global__ void __launch_bounds__(kThreads, kSweepCtasPerSm) sweep_spmv_kernel(SweepOp op, const double* v, int p,
+                                                                             double* out) {
+  __shared__ SweepSmem sm;
+  const int b = blockIdx.x;
+  const int r0 = b * kSweepRows + threadIdx.x;
+  double acc[kSweepRPT];
+  const unsigned has = sweep_block(op, p, b, v, acc, sm);
+  const bool last = p == op.panels - 1;
+#pragma unroll
+  for (int q = 0; q < kSweepRPT; ++q) {
+    const int r = r0 + q * kThreads;
+    if (r >= op.rows) continue;
+    if (last)
+      out[r] = acc[q];
+    else if (p == 0 || ((has >> q) & 1u))
+      st_acc(op.acc + r, acc[q]);
+  }
+}
+
+void panel_kernel_attributes() {}
 
 namespace {
 template <class... P, class... A>
@@ -266,24 +467,29 @@ void launch_pdl2(void (*kern)(P...), int grid, size_t smem, cudaStream_t s, A&&.
 }
 }  // namespace
 
-int panel_combine_blocks(int rows) { return (rows + kIterGeom.stream_rows - 1) / kIterGeom.stream_rows; }
-
-void launch_panel_dual(const DevCsr& kp, int panels, double* partial, const DevIter& it, cudaStream_t s) {
-  const size_t sm = stream_smem_bytes<PartialEpi>();
-  launch_pdl2(panel_spmv_kernel<false>, kp.ntiles, sm, s, kp, it, partial, -1);
-  launch_pdl2(dual_combine_kernel, 1 + panel_combine_blocks(it.m), 0, s, it, (const double*)partial, panels);
+void launch_panel_dual(const PanelView& kp, const DevIter& it, cudaStream_t s) {
+  const SweepOp& op = kp;
+  for (int p = 0; p + 1 < op.panels; ++p) launch_pdl2(sweep_pass_kernel<false>, op.nblk, 0, s, op, it, p, -1);
+  launch_pdl2(sweep_dual_final_kernel, 1 + op.nblk, 0, s, op, it);
 }
 
-void launch_panel_primal(const DevCsr& ktp, int panels, double* partial, const DevIter& it, int mode_override,
-                         cudaStream_t s) {
-  const size_t sm = stream_smem_bytes<PartialEpi>();
-  launch_pdl2(panel_spmv_kernel<true>, ktp.ntiles, sm, s, ktp, it, partial, mode_override);
-  const int nblk = panel_combine_blocks(it.n);
-  const int grid = nblk + it.avg_blocks;
+void launch_panel_primal(const PanelView& ktp, const DevIter& it, int mode_override, cudaStream_t s) {
+  const SweepOp& op = ktp;
+  for (int p = 0; p + 1 < op.panels; ++p)
+    launch_pdl2(sweep_pass_kernel<true>, op.nblk, 0, s, op, it, p, mode_override);
+  const int grid = op.nblk + it.avg_blocks;
   if (it.nonneg)
-    launch_pdl2(primal_combine_kernel<true>, grid, 0, s, it, (const double*)partial, panels, nblk, mode_override);
+    launch_pdl2(sweep_primal_final_kernel<true>, grid, 0, s, op, it, mode_override);
   else
-    launch_pdl2(primal_combine_kernel<false>, grid, 0, s, it, (const double*)partial, panels, nblk, mode_override);
+    launch_pdl2(sweep_primal_final_kernel<false>, grid, 0, s, op, it, mode_override);
+}
+
+void launch_panel_spmv(const PanelView& pv, const double* v, double* out, cudaStream_t s) {
+  const SweepOp& op = pv;
+  for (int p = 0; p < op.panels; ++p) {
+    sweep_spmv_kernel<<<op.nblk, kThreads, 0, s>>>(op, v, p, out);
+    PDLP_CUDA(cudaGetLastError());
+  }
 }
 
 }  // namespace pdlp

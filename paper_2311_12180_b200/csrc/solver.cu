@@ -57,9 +57,11 @@ void validate_params(const pdlp_params& p) {  // SolverParams::validate, solver.
     invalid("params: the persistent engine runs on one device (world_size 1)");
 }
 
-// GeneralFormLp::validate (lp_model.hpp:45-72), then SolverParams::validate;
-// runs before any CUDA call so invalid input is PDLP_EINVAL even without a GPU.
-void validate_input(const pdlp_lp& lp, const pdlp_params& params) {
+}  // namespace
+
+// GeneralFormLp::validate (lp_model.hpp:45-72) plus the raw-array checks of the
+// C ABI (present pointers, monotone row offsets); host only, no CUDA call.
+void validate_lp(const pdlp_lp& lp) {
   const pdlp_csr& G = lp.inequality_matrix;
   const pdlp_csr& A = lp.equality_matrix;
   const int64_t n = lp.num_variables;
@@ -81,6 +83,9 @@ void validate_input(const pdlp_lp& lp, const pdlp_params& params) {
     if (c->num_rows > 0 && !c->row_offsets) invalid("lp: missing row offsets");
     if (c->row_offsets && (c->row_offsets[0] != 0 || c->row_offsets[c->num_rows] != c->nnz))
       invalid("csr: row_offsets must start at 0 and end at nnz");
+    if (c->row_offsets)
+      for (int64_t r = 0; r < c->num_rows; ++r)
+        if (c->row_offsets[r + 1] < c->row_offsets[r]) invalid("csr: row_offsets must be non-decreasing");
   }
   for (int64_t i = 0; i < n; ++i) {
     const double l = lp.lower[i], u = lp.upper[i];
@@ -90,7 +95,18 @@ void validate_input(const pdlp_lp& lp, const pdlp_params& params) {
   }
   for (int64_t i = 0; i < n; ++i)
     if (std::isnan(lp.objective[i])) invalid("lp: NaN objective entry");
+}
+
+namespace {
+
+// validate_lp, then SolverParams::validate; runs before any CUDA call so
+// invalid input is PDLP_EINVAL even without a GPU.
+void validate_input(const pdlp_lp& lp, const pdlp_params& params) {
+  validate_lp(lp);
   validate_params(params);
+  const int64_t n = lp.num_variables;
+  const int64_t m = lp.inequality_matrix.num_rows + lp.equality_matrix.num_rows;
+  const int64_t nnz = lp.inequality_matrix.nnz + lp.equality_matrix.nnz;
   const int64_t lim = int64_t(std::numeric_limits<int32_t>::max()) - 1024;
   if (n > lim || m > lim || nnz > lim)
     throw std::runtime_error("instance exceeds the 32-bit index layout of one device (shard it)");
@@ -345,8 +361,8 @@ void Solver::setup(const pdlp_lp& lp) {
   // column panels for operators that scatter over a vector much larger than
   // L2 (fast mode, one device; panels.cu)
   if (!parity() && world_ == 1 && !(std::getenv("PDLP_PANELS") && std::atoi(std::getenv("PDLP_PANELS")) == 0)) {
-    build_panels(kpan_, kpan_plan_, K_, int(m_), int(n_), "K");
-    build_panels(ktpan_, ktpan_plan_, KT_, int(n_), int(m_), "KT");
+    build_panels(kpan_, K_, int(m_), int(n_), "K");
+    build_panels(ktpan_, KT_, int(n_), int(m_), "KT");
   }
   mark("plans");
   allocate_iteration();
@@ -357,18 +373,28 @@ void Solver::setup(const pdlp_lp& lp) {
 }
 
 // Decides whether `op` (rows x cols) gets column panels and builds them: the
-// gathered vector must exceed the L2 budget (48 MB per panel) and the rows must
-// scatter over it (on average across at least half of min(panels, row length)
-// panels, i.e. no locality a single pass could use). PDLP_PANELS=1 forces
+// gathered vector must exceed one panel's L2 budget (PDLP_PANEL_MB, default
+// 48 MB) and the rows must scatter over it (on average across at least half of
+// min(panels, row length) panels, i.e. no locality a single pass could use);
+// no row may hold more than 255 entries in one panel. PDLP_PANELS=1 forces
 // panels of PDLP_PANEL_WIDTH columns (tests); =0 disables them.
-void Solver::build_panels(PanelOp& po, OpPlan& plan, const DevCsr& op, int rows, int cols,
-                          const char* which) {
+void Solver::build_panels(PanelOp& po, const DevCsr& op, int rows, int cols, const char* which) {
   cudaStream_t s = stream_;
   const char* force = std::getenv("PDLP_PANELS");
   const bool forced = force && std::atoi(force) == 1;
-  int width = int(std::max<int64_t>(1, (int64_t(48) << 20) / 8));
-  if (forced && std::getenv("PDLP_PANEL_WIDTH")) width = std::max(1, std::atoi(std::getenv("PDLP_PANEL_WIDTH")));
-  const int panels = int((int64_t(cols) + width - 1) / width);
+  // measured on C4 (tools/panel_sweep.py): K (x, 320 MB) is fastest in 48 MB
+  // panels; K^T has twice the rows, so its per-panel running sums cost twice
+  // as much and it is fastest in 64 MB panels of y
+  const bool kt = std::strcmp(which, "KT") == 0;
+  double budget_mb = kt ? 64.0 : 48.0;
+  if (const char* e = std::getenv("PDLP_PANEL_MB")) budget_mb = std::max(1.0, std::atof(e));
+  if (const char* e = std::getenv(kt ? "PDLP_PANEL_MB_T" : "PDLP_PANEL_MB_K")) budget_mb = std::max(1.0, std::atof(e));
+  int panels = int(std::ceil(8.0 * double(cols) / (budget_mb * 1048576.0)));
+  int width = std::max(1, int((int64_t(cols) + panels - 1) / std::max(1, panels)));
+  if (forced && std::getenv("PDLP_PANEL_WIDTH")) {
+    width = std::max(1, std::atoi(std::getenv("PDLP_PANEL_WIDTH")));
+    panels = int((int64_t(cols) + width - 1) / width);
+  }
   if (panels < 2 || rows < 1 || op.nnz < 1) return;
   if (int64_t(panels) * rows >= int64_t(std::numeric_limits<int32_t>::max()) - 1024) return;
   if (!forced) {
@@ -382,13 +408,16 @@ void Solver::build_panels(PanelOp& po, OpPlan& plan, const DevCsr& op, int rows,
     const double avg_len = double(op.nnz) / double(rows);
     if (per_row < 0.5 * std::min(double(panels), avg_len)) return;
   }
-  // stacked CSR: entry k of row r, column c goes to stacked row (c / width) * rows + r;
-  // a stable radix sort keeps each row's columns in increasing order
+  // panel-major order: entry k of row r, column c goes to stacked row
+  // (c / width) * rows + r; a stable radix sort keeps each row's columns in
+  // increasing order
   const int64_t nnz = op.nnz;
   const int srows = panels * rows;
+  const int rows_pad = panel_rows_pad(rows);
+  const int nblk = panel_blocks(rows);
   DevBuf<int> row_of{static_cast<size_t>(nnz)}, keys{static_cast<size_t>(nnz)},
       keys2{static_cast<size_t>(nnz)}, ids{static_cast<size_t>(nnz)}, perm{static_cast<size_t>(nnz)},
-      counts{static_cast<size_t>(srows) + 1};
+      counts{static_cast<size_t>(srows) + 1}, so{static_cast<size_t>(srows) + 1};
   launch_expand_rows(op.rp, rows, row_of.get(), s);
   launch_panel_keys(row_of.get(), op.col, nnz, width, rows, keys.get(), s);
   launch_iota(ids.get(), nnz, s);
@@ -397,45 +426,57 @@ void Solver::build_panels(PanelOp& po, OpPlan& plan, const DevCsr& op, int rows,
   size_t tmp_bytes = 0;
   PDLP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys.get(), keys2.get(), ids.get(), perm.get(),
                                             int(nnz), 0, end_bit, s));
+  // (temporaries are freed on cudaStreamPerThread: they must outlive the work
+  // queued on `s`, which is synchronised before they go out of scope)
   DevBuf<unsigned char> tmp{tmp_bytes};
   PDLP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tmp_bytes, keys.get(), keys2.get(), ids.get(), perm.get(),
                                             int(nnz), 0, end_bit, s));
   counts.zero(s);
   launch_count_cols(keys.get(), nnz, counts.get(), s);
-  po.rp.alloc(size_t(srows) + 1 + kVecPad);
-  po.rp.zero(s);
   size_t scan_bytes = 0;
-  PDLP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, counts.get(), po.rp.get(), srows + 1, s));
+  PDLP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, counts.get(), so.get(), srows + 1, s));
   DevBuf<unsigned char> scan_tmp{scan_bytes};
-  PDLP_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp.get(), scan_bytes, counts.get(), po.rp.get(), srows + 1, s));
+  PDLP_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp.get(), scan_bytes, counts.get(), so.get(), srows + 1, s));
+  po.cnt.alloc(size_t(panels) * rows_pad);
+  po.boff.alloc(size_t(panels) * (nblk + 1));
+  DevBuf<int> over{static_cast<size_t>(1)};
+  over.zero(s);
+  launch_panel_meta(counts.get(), so.get(), rows, rows_pad, panels, nblk, po.cnt.get(), po.boff.get(), over.get(),
+                    s);
+  int over_h = 0;
+  PDLP_CUDA(cudaMemcpyAsync(&over_h, over.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  PDLP_CUDA(cudaStreamSynchronize(s));
+  if (over_h) {  // a row holds more than 255 entries of one panel: no panels
+    po.cnt = DevBuf<unsigned char>();
+    po.boff = DevBuf<int>();
+    return;
+  }
   po.col.alloc(size_t(nnz) + kVecPad);
   po.val.alloc(size_t(nnz) + kVecPad);
   po.col.zero(s);
   po.val.zero(s);
   launch_panel_gather(perm.get(), op.col, op.val, nnz, po.col.get(), po.val.get(), s);
-  std::vector<int> rp_h(size_t(srows) + 1);
-  PDLP_CUDA(cudaMemcpyAsync(rp_h.data(), po.rp.get(), rp_h.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
   PDLP_CUDA(cudaStreamSynchronize(s));
-  const DevCsr base{po.rp.get(), po.col.get(), po.val.get(), nullptr, srows, cols, nnz};
-  build_plan(plan, base, rp_h, kPanelGeom, {}, 0, srows);
-  po.partial.alloc(size_t(srows));
+  po.acc.alloc(size_t(rows) + kVecPad);
   po.panels = panels;
   po.width = width;
+  po.view = PanelView{po.col.get(), po.val.get(), po.cnt.get(), po.boff.get(), po.acc.get(),
+                      rows, rows_pad, nblk, panels};
   if (std::getenv("PDLP_TRACE_SETUP"))
-    std::fprintf(stderr, "[pdlp setup] %s: %d column panels of %d, %d tiles\n", which, panels, width,
-                 plan.csr.ntiles);
+    std::fprintf(stderr, "[pdlp setup] %s: %d column panels of %d columns, %d row blocks\n", which, panels,
+                 width, nblk);
 }
 
 void Solver::dual_step(unsigned long long cond, int use_cond) {
   if (kpan_.panels)
-    launch_panel_dual(kpan_plan_.csr, kpan_.panels, kpan_.partial.get(), it_, stream_);
+    launch_panel_dual(kpan_.view, it_, stream_);
   else
     launch_dual(K_, it_, parity(), cond, use_cond, stream_);
 }
 
 void Solver::primal_step(int mode_override, unsigned long long cond, int use_cond) {
   if (ktpan_.panels)
-    launch_panel_primal(ktpan_plan_.csr, ktpan_.panels, ktpan_.partial.get(), it_, mode_override, stream_);
+    launch_panel_primal(ktpan_.view, it_, mode_override, stream_);
   else
     launch_primal(KT_, it_, parity(), mode_override, stream_, cond, use_cond);
 }
@@ -644,8 +685,8 @@ void Solver::allocate_iteration() {
   const int p_grid = KT_.ntiles + avg_blocks;
   // partial counts: one per tile of the operator's kernel, or one per combine
   // block when the operator runs as column panels
-  const int k_tiles = kpan_.panels ? panel_combine_blocks(int(m_)) : int(k_it_.plan.tiles.size());
-  const int kt_tiles = ktpan_.panels ? panel_combine_blocks(int(n_)) : int(kt_it_.plan.tiles.size());
+  const int k_tiles = kpan_.panels ? kpan_.view.nblk : int(k_it_.plan.tiles.size());
+  const int kt_tiles = ktpan_.panels ? ktpan_.view.nblk : int(kt_it_.plan.tiles.size());
   d_part_.alloc(size_t(k_tiles) * 3, ipc);
   p_part_.alloc(size_t(kt_tiles) * 4 + 2, ipc);  // two parity buffers + dx^2 total
   p_part_.zero(s);
@@ -1508,7 +1549,13 @@ void Solver::spmv(int op, const double* in, double* out) {
   const int64_t nin = transpose ? m_ : n_, nout = transpose ? n_ : m_;
   DevBuf<double> din(nin), dout(nout);
   if (nin) PDLP_CUDA(cudaMemcpyAsync(din.get(), in, nin * 8, cudaMemcpyHostToDevice, stream_));
-  launch_spmv(transpose ? KT_full_ : K_full_, orig, din.get(), dout.get(), parity(), stream_);
+  // the scaled operator through the engine the iteration uses (column panels
+  // when the operator is panelized)
+  const PanelOp& po = transpose ? ktpan_ : kpan_;
+  if (!orig && po.panels)
+    launch_panel_spmv(po.view, din.get(), dout.get(), stream_);
+  else
+    launch_spmv(transpose ? KT_full_ : K_full_, orig, din.get(), dout.get(), parity(), stream_);
   if (nout) PDLP_CUDA(cudaMemcpyAsync(out, dout.get(), nout * 8, cudaMemcpyDeviceToHost, stream_));
   PDLP_CUDA(cudaStreamSynchronize(stream_));
 }
@@ -1528,11 +1575,19 @@ void Solver::time_kernel(int which, int reps, double* avg_ms, double* bytes) {
     cudaEvent_t e0, e1;
     PDLP_CUDA(cudaEventCreate(&e0));
     PDLP_CUDA(cudaEventCreate(&e1));
+    // the operator as the iteration runs it: panel sweeps when panelized
     auto run = [&]() {
-      if (which == 2)
-        launch_spmv(K_, false, it_.x[st.ix_cur], it_.kx[1 - st.ikx_cur], parity(), stream_);
-      else
-        launch_spmv(KT_, false, it_.y[st.iy_cur], it_.kty[1 - st.ikty_cur], parity(), stream_);
+      if (which == 2) {
+        if (kpan_.panels)
+          launch_panel_spmv(kpan_.view, it_.x[st.ix_cur], it_.kx[1 - st.ikx_cur], stream_);
+        else
+          launch_spmv(K_, false, it_.x[st.ix_cur], it_.kx[1 - st.ikx_cur], parity(), stream_);
+      } else {
+        if (ktpan_.panels)
+          launch_panel_spmv(ktpan_.view, it_.y[st.iy_cur], it_.kty[1 - st.ikty_cur], stream_);
+        else
+          launch_spmv(KT_, false, it_.y[st.iy_cur], it_.kty[1 - st.ikty_cur], parity(), stream_);
+      }
     };
     run();
     PDLP_CUDA(cudaEventRecord(e0, stream_));
@@ -1544,9 +1599,7 @@ void Solver::time_kernel(int which, int reps, double* avg_ms, double* bytes) {
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     if (avg_ms) *avg_ms = ms / reps;
-    const double nnz = double(nnz_), rows = double(which == 2 ? m_ : n_),
-                 cols = double(which == 2 ? n_ : m_);
-    if (bytes) *bytes = 12.0 * nnz + 4.0 * (rows + 1) + 8.0 * cols + 8.0 * rows;
+    if (bytes) kernel_bytes(which, bytes, nullptr);
     state_valid_ = false;
     return;
   }
@@ -1589,15 +1642,43 @@ void Solver::time_kernel(int which, int reps, double* avg_ms, double* bytes) {
   download_state();
   state_valid_ = false;
   if (avg_ms) *avg_ms = total / reps;
+  if (bytes) kernel_bytes(which, bytes, nullptr);
+}
+
+// Bytes of one launch of kernel `which` (0 dual, 1 primal accept, 2 SpMV K x,
+// 3 SpMV K^T y). `alg`: SURVEY.md §8(d)'s algorithmic figure (int32 index +
+// fp64 value per nonzero, int32 row offsets, the gathered vector once, every
+// dense stream once). `moved`: what the variant the iteration launches moves
+// when each access reaches DRAM once: bounds only when not all [0, +inf),
+// K'y' only when stored (not kty_lazy), and for column panels the per-panel
+// row counts and block offsets instead of row offsets plus the running row
+// sums (written by the first pass, read and written by the middle ones, read
+// by the last).
+void Solver::kernel_bytes(int which, double* alg, double* moved) const {
   const double nnz = double(nnz_), n = double(n_), m = double(m_);
-  if (bytes) {
-    // algorithmic bytes of one launch: int32 index + fp64
-    // value per nonzero, int32 offsets, each dense stream touched once
-    if (which == 0)
-      *bytes = 12.0 * nnz + 4.0 * (m + 1) + 8.0 * n + 8.0 * 5.0 * m;
-    else
-      *bytes = 12.0 * nnz + 4.0 * (n + 1) + 8.0 * m + 8.0 * 8.0 * n + 8.0 * 3.0 * m;
+  const bool dual_side = which == 0 || which == 2;
+  const double rows = dual_side ? m : n, cols = dual_side ? n : m;
+  const PanelOp& po = dual_side ? kpan_ : ktpan_;
+  double a = 12.0 * nnz + 4.0 * (rows + 1) + 8.0 * cols;
+  double mv = 12.0 * nnz + 8.0 * cols;
+  if (po.panels) {
+    const double P = po.panels;
+    mv += P * double(po.view.rows_pad) + 4.0 * P * (po.view.nblk + 1) + 16.0 * rows * (P - 1.0);
+  } else {
+    mv += 4.0 * (rows + 1);
   }
+  double dense_a = 0.0, dense_mv = 0.0;
+  if (which == 0) {  // y, q, Kx read; y', Kx' write
+    dense_a = dense_mv = 8.0 * 5.0 * m;
+  } else if (which == 1) {  // x, c, l, u read; K'y', x' write; avg_x r+w; avg_y r+w, y read
+    dense_a = 8.0 * 8.0 * n + 8.0 * 3.0 * m;
+    const double nstreams = 5.0 + (it_.nonneg ? 0.0 : 2.0) + (it_.kty_lazy ? 0.0 : 1.0);
+    dense_mv = 8.0 * nstreams * n + 8.0 * 3.0 * m;
+  } else {  // plain SpMV: the output once
+    dense_a = dense_mv = 8.0 * rows;
+  }
+  if (alg) *alg = a + dense_a;
+  if (moved) *moved = mv + dense_mv;
 }
 
 void Solver::sizes(int64_t* out) const {

@@ -20,6 +20,10 @@
 
 namespace pdlp {
 
+// GeneralFormLp::validate plus the C ABI's raw-array checks (host only).
+void validate_lp(const pdlp_lp& lp);
+
+
 template <class T>
 class DevBuf {
  public:
@@ -188,6 +192,8 @@ class Solver {
   void get_scaling(double* row_scale, double* col_scale) const;
   void spmv(int op, const double* in, double* out);
   void time_kernel(int which, int reps, double* avg_ms, double* bytes);
+  void kernel_bytes(int which, double* alg, double* moved) const;
+  int panels(int op) const { return op == 0 ? kpan_.panels : ktpan_.panels; }
   void sizes(int64_t* out) const;
   // ---- sharding ----
   static void link_local(const std::vector<Solver*>& ranks);
@@ -211,15 +217,17 @@ class Solver {
                   const std::vector<int64_t>& breaks, int64_t r0, int64_t r1,
                   const std::vector<uint8_t>* contig = nullptr);
   void shard_view_upload();
-  // column panels of one operator (panels.cu): stacked CSR, its plan, partials
+  // column panels of one operator (panels.cu): panel-major entries, per-panel
+  // row counts and block offsets, running row sums
   struct PanelOp {
     int panels = 0;  // 0: not panelized
     int width = 0;
-    DevBuf<int> rp, col;
-    DevBuf<double> val;
-    DevBuf<double> partial;  // [panels][rows]
+    DevBuf<int> col, boff;
+    DevBuf<double> val, acc;
+    DevBuf<unsigned char> cnt;
+    PanelView view{};
   };
-  void build_panels(PanelOp& po, OpPlan& plan, const DevCsr& op, int rows, int cols, const char* which);
+  void build_panels(PanelOp& po, const DevCsr& op, int rows, int cols, const char* which);
   void dual_step(unsigned long long cond, int use_cond);
   void primal_step(int mode_override, unsigned long long cond = 0, int use_cond = 0);
   void phase() {
@@ -262,7 +270,6 @@ class Solver {
   DevBuf<double> k_val_, k_val_orig_, kt_val_, kt_val_orig_;
   OpPlan k_it_, kt_it_, k_win_, kt_win_, k_ev_, kt_ev_;
   PanelOp kpan_, ktpan_;
-  OpPlan kpan_plan_, ktpan_plan_;
   DevCsr K_{}, KT_{};  // the iteration-kernel tilings (this rank's tiles)
   DevCsr K_full_{}, KT_full_{};  // every tile (kernel-level API on a sharded rank)
 

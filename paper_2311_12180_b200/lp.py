@@ -175,7 +175,15 @@ class GeneralFormLp:
         return self.inequality_matrix.nnz + self.equality_matrix.nnz
 
     def validate(self) -> None:
-        """GeneralFormLp::validate (lp_model.hpp:45-72)."""
+        """GeneralFormLp::validate (lp_model.hpp:45-72), plus the CSR storage
+        checks the raw-pointer C ABI needs."""
+        for name, M in (("inequality", self.inequality_matrix), ("equality", self.equality_matrix)):
+            if M.row_offsets.size != M.num_rows + 1:
+                raise ValueError(f"lp: {name} matrix row_offsets must have num_rows + 1 entries")
+            if M.col_indices.size != M.values.size:
+                raise ValueError(f"lp: {name} matrix col_indices and values differ in length")
+            if M.num_rows >= 0 and (M.row_offsets[0] != 0 or M.row_offsets[-1] != M.values.size):
+                raise ValueError(f"lp: {name} matrix row_offsets must run from 0 to nnz")
         n = self.num_variables
         if self.inequality_matrix.num_cols != n or self.equality_matrix.num_cols != n:
             raise ValueError("lp: constraint matrices must have n columns")

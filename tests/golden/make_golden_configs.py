@@ -1,0 +1,105 @@
+"""Golden vectors of the BASELINE.json configurations from the REFERENCE
+solver (oracle/_ref, the unmodified pdhglp headers built by oracle/Makefile).
+Run in the build container only (the GPU box has no /root/reference):
+
+    make -C oracle ref && python tests/golden/make_golden_configs.py [C2 C3 C4]
+
+Outputs (committed), per config, configs_<name>.npz + an entry in
+configs.json:
+  * the instance hash (generators.config(name) is seeded and deterministic);
+  * the first N iterates of the re-driven SolveLoop::run (solver.hpp:759-929;
+    N = 100 for C2 and C3, 20 for C4): counters (total, inner, trials), eta,
+    eta_hat, omega, the 2-norm and max-norm of x and y, and the values of x
+    and y at a fixed seeded sample of indices (full vectors are 8-320 MB per
+    iterate);
+  * C2 only: the reference's full solve at eps 1e-4 and 1e-8 (solve(),
+    solver.hpp:935-940): status, iterations, restarts, objectives.
+"""
+from __future__ import annotations
+
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[2]
+sys.path.insert(0, str(ROOT))
+
+from oracle import oracle as O  # noqa: E402
+from paper_2311_12180_b200 import SolverParams, generators  # noqa: E402
+from tests.helpers import lp_hash  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+ITERATES = {"C2": 100, "C3": 100, "C4": 20}
+SAMPLES = 16384
+SAMPLE_SEED = 20261017
+# C2 and C3 are compared against a live reference session on full vectors;
+# their goldens only pin that session, so they keep every 8th sample
+SAMPLE_STRIDE = {"C2": 8, "C3": 8, "C4": 1}
+
+
+def sample_indices(size: int, seed: int) -> np.ndarray:
+    if size <= SAMPLES:
+        return np.arange(size, dtype=np.int64)
+    return np.sort(np.random.default_rng(seed).choice(size, SAMPLES, replace=False)).astype(np.int64)
+
+
+def iterates(name: str, lp) -> dict:
+    n, m = lp.num_variables, lp.num_constraints
+    st = SAMPLE_STRIDE[name]
+    ix, iy = sample_indices(n, SAMPLE_SEED)[::st], sample_indices(m, SAMPLE_SEED + 1)[::st]
+    t = time.time()
+    s = O.Session(lp, SolverParams(), "ref")
+    print(f"{name}: reference setup {time.time() - t:.1f} s", flush=True)
+    N = ITERATES[name]
+    rec = {k: [] for k in ("total", "inner", "trials", "eta", "eta_hat", "omega", "x_norm", "y_norm", "x_max",
+                           "y_max", "x_s", "y_s")}
+    t = time.time()
+    for _ in range(N):
+        s.run(1)
+        it = s.iterate()
+        for k in ("total", "inner", "trials", "eta", "eta_hat", "omega"):
+            rec[k].append(it[k])
+        rec["x_norm"].append(np.linalg.norm(it["x"]))
+        rec["y_norm"].append(np.linalg.norm(it["y"]))
+        rec["x_max"].append(np.abs(it["x"]).max())
+        rec["y_max"].append(np.abs(it["y"]).max())
+        rec["x_s"].append(it["x"][ix])
+        rec["y_s"].append(it["y"][iy])
+    s.close()
+    print(f"{name}: {N} iterates in {time.time() - t:.1f} s", flush=True)
+    out = {k: np.asarray(v) for k, v in rec.items()}
+    out["ix"], out["iy"] = ix, iy
+    return out
+
+
+def main() -> None:
+    names = sys.argv[1:] or ["C2", "C3", "C4"]
+    meta_path = OUT / "configs.json"
+    meta = json.loads(meta_path.read_text()) if meta_path.exists() else {}
+    for name in names:
+        t = time.time()
+        lp = generators.config(name)
+        entry = {"instance_sha256": lp_hash(lp), "n": lp.num_variables, "m": lp.num_constraints,
+                 "nnz": lp.nnz, "seed": generators.SEEDS[name], "iterates": ITERATES[name]}
+        print(f"{name}: generated in {time.time() - t:.1f} s", flush=True)
+        np.savez_compressed(OUT / f"configs_{name}.npz", **iterates(name, lp))
+        if name == "C2":
+            for eps in (1e-4, 1e-8):
+                t = time.time()
+                r = O.solve(lp, SolverParams(eps_optimal=eps), "ref")
+                entry[f"solve_{eps:g}"] = {"status": str(r.status), "iterations": r.iterations,
+                                           "restarts": r.restarts,
+                                           "primal_objective": r.info["primal_objective"],
+                                           "dual_objective": r.info["dual_objective"],
+                                           "seconds": time.time() - t}
+                print(f"{name}: solve {eps:g}: {entry[f'solve_{eps:g}']}", flush=True)
+        meta[name] = entry
+        meta_path.write_text(json.dumps(meta, indent=1, sort_keys=True) + "\n")
+        del lp
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,158 @@
+"""Parity on the BASELINE.json configurations at their real sizes (fast mode,
+the product's default) against the reference solver.
+
+* C2 (configs[1], 1k x 1k transportation): the full solve at 1e-4 and 1e-8
+  against the reference's own solve (tests/golden/configs.json, made by
+  tests/golden/make_golden_configs.py from oracle/_ref): same status,
+  objectives within the solve tolerance, and the reference's termination
+  check (solver.hpp:204-222, recomputed by oracle/_ref) passing at the GPU's
+  point.
+* C2 and C3 (configs[2], multicommodity flow, 20M nonzeros): the first 100
+  iterates against a live reference session on the box (oracle/_ref, the
+  re-driven SolveLoop::run, solver.hpp:759-929), full vectors, relative
+  error <= 1e-10 in the 2-norm and in the max-norm (north_star's bar);
+  counters equal. The live session is first pinned to the committed goldens.
+* C4 (configs[3], 200M nonzeros): the first 20 iterates against the
+  committed goldens (sampled entries and full-vector norms).
+* C3, C4, C5 solved to 1e-4: the reference's termination check at the
+  GPU's returned point (acceptance criterion 2 style, acceptance_main.cpp:
+  79-154).
+"""
+from __future__ import annotations
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2311_12180_b200 import Solver, SolverParams, SolveStatus, generators, solve
+from tests.helpers import GOLDEN, lp_hash
+
+pytestmark = pytest.mark.gpu
+
+BAR = 1e-10  # north_star: the first 100 iterates within 1e-10 relative
+
+
+def meta() -> dict:
+    return json.loads((GOLDEN / "configs.json").read_text())
+
+
+def golden(name: str) -> dict:
+    return dict(np.load(GOLDEN / f"configs_{name}.npz"))
+
+
+def ref_kind() -> str:
+    if not O.available("ref"):
+        pytest.skip("oracle/_ref not built")
+    return "ref"
+
+
+def rel2(a, b) -> float:
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def relinf(a, b) -> float:
+    return float(np.abs(a - b).max(initial=0.0) / max(np.abs(b).max(initial=0.0), 1e-300))
+
+
+# ---------------------------------------------------------------------------
+# C2: full solves
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("eps", [1e-4, 1e-8])
+def test_c2_solve_matches_reference(eps):
+    lp = generators.config("C2")
+    ref = meta()["C2"]
+    assert lp_hash(lp) == ref["instance_sha256"]
+    want = ref[f"solve_{eps:g}"]
+    r = solve(lp, SolverParams(eps_optimal=eps))
+    assert str(r.status) == want["status"] == "optimal"
+    obj, robj = r.info["primal_objective"], want["primal_objective"]
+    # both points meet the relative gap at eps, so their objectives agree to about eps
+    assert abs(obj - robj) <= 2.0 * eps * (1.0 + abs(robj)), (obj, robj)
+    chk = O.check_termination(lp, r.point.primal, r.point.dual, eps, ref_kind())
+    assert chk["terminated"], chk
+    # iteration counts: fast mode differs only in reduction order, which moves the
+    # restart sequence; recorded, and bounded loosely
+    print(f"C2 eps {eps:g}: {r.iterations} iterations (reference {want['iterations']}), obj {obj!r} vs {robj!r}")
+    assert r.iterations <= 2 * want["iterations"]
+
+
+# ---------------------------------------------------------------------------
+# first iterates, full vectors, against a live reference session
+# ---------------------------------------------------------------------------
+
+def check_against_golden(g: dict, k: int, it: dict, tol: float) -> None:
+    for key in ("total", "inner", "trials"):
+        assert it[key] == g[key][k], (key, k, it[key], g[key][k])
+    for key in ("eta", "eta_hat", "omega"):
+        assert abs(it[key] - g[key][k]) <= tol * abs(g[key][k]), (key, k)
+    xs, ys = it["x"][g["ix"]], it["y"][g["iy"]]
+    assert relinf(xs, g["x_s"][k]) <= tol and relinf(ys, g["y_s"][k]) <= tol, k
+    assert abs(np.linalg.norm(it["x"]) - g["x_norm"][k]) <= tol * g["x_norm"][k]
+    assert abs(np.linalg.norm(it["y"]) - g["y_norm"][k]) <= tol * max(g["y_norm"][k], 1e-300)
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_first_100_iterates_full_vectors(name):
+    lp = generators.config(name)
+    assert lp_hash(lp) == meta()[name]["instance_sha256"]
+    g = golden(name)
+    ref = O.Session(lp, SolverParams(), ref_kind())
+    worst2 = worstinf = 0.0
+    with Solver(lp, SolverParams()) as s:
+        s.iterate_begin()
+        for k in range(int(meta()[name]["iterates"])):
+            s.iterate_run(1)
+            ref.run(1)
+            a, b = s.iterate(), ref.iterate()
+            check_against_golden(g, k, b, 0.0)  # the live reference is the committed one, bitwise
+            assert (a["total"], a["inner"], a["trials"]) == (b["total"], b["inner"], b["trials"]), k
+            za, zb = np.concatenate([a["x"], a["y"]]), np.concatenate([b["x"], b["y"]])
+            worst2 = max(worst2, rel2(za, zb), rel2(a["x"], b["x"]), rel2(a["y"], b["y"]))
+            worstinf = max(worstinf, relinf(za, zb), relinf(a["x"], b["x"]), relinf(a["y"], b["y"]))
+    ref.close()
+    print(f"{name}: worst relative error over the first iterates: 2-norm {worst2:.3e}, max-norm {worstinf:.3e}")
+    assert worst2 <= BAR and worstinf <= BAR, (worst2, worstinf)
+
+
+def test_c4_first_20_iterates_against_goldens():
+    lp = generators.config("C4")
+    m = meta()["C4"]
+    assert lp_hash(lp) == m["instance_sha256"]
+    g = golden("C4")
+    worst = 0.0
+    with Solver(lp, SolverParams()) as s:
+        del lp
+        s.iterate_begin()
+        for k in range(int(m["iterates"])):
+            s.iterate_run(1)
+            a = s.iterate()
+            for key in ("total", "inner", "trials"):
+                assert a[key] == g[key][k], (key, k)
+            xs, ys = a["x"][g["ix"]], a["y"][g["iy"]]
+            errs = [relinf(xs, g["x_s"][k]), relinf(ys, g["y_s"][k]),
+                    abs(np.linalg.norm(a["x"]) - g["x_norm"][k]) / g["x_norm"][k],
+                    abs(np.linalg.norm(a["y"]) - g["y_norm"][k]) / max(g["y_norm"][k], 1e-300),
+                    abs(a["eta"] - g["eta"][k]) / g["eta"][k], abs(a["omega"] - g["omega"][k]) / g["omega"][k]]
+            worst = max(worst, *errs)
+    print(f"C4: worst relative error over 20 iterates (sampled max-norm, norms, eta, omega): {worst:.3e}")
+    assert worst <= BAR, worst
+
+
+# ---------------------------------------------------------------------------
+# the reference's termination check at the GPU's final points
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+def test_final_point_passes_reference_termination_check(name):
+    if name == "C5" and os.environ.get("PDLP_TEST_C5", "1") == "0":
+        pytest.skip("PDLP_TEST_C5=0")
+    lp = generators.config(name)
+    r = solve(lp, SolverParams(eps_optimal=1e-4, time_limit_seconds=600.0))
+    assert r.status == SolveStatus.OPTIMAL, r.status
+    chk = O.check_termination(lp, r.point.primal, r.point.dual, 1e-4, ref_kind())
+    print(f"{name}: {r.iterations} iterations, reference check {chk}")
+    assert chk["terminated"], chk

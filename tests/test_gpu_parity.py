@@ -454,6 +454,29 @@ def test_gpu_from_triplets_large_matches_host_csr():
 # column panels (panels.cu): forced on small instances with narrow panels
 # ---------------------------------------------------------------------------
 
+@pytest.mark.parametrize("width", ["700", "4096"])
+def test_column_panel_spmv_bitwise_sequential(width, monkeypatch):
+    """The panel sweep sums every row by one thread in column order, from 0.0:
+    bitwise equal to the reference's sequential spmv (sparse_matrix.hpp:117-132)
+    over K and to spmv_transpose (:142-158) over the stored K^T."""
+    monkeypatch.setenv("PDLP_PANELS", "1")
+    monkeypatch.setenv("PDLP_PANEL_WIDTH", width)
+    lp = generators.config("C1")
+    rng = np.random.default_rng(5)
+    K = stacked_k(lp)
+    lens = np.diff(K.row_offsets)
+    with Solver(lp, SolverParams()) as s:
+        d1, d2 = s.scaling()
+        x = rng.uniform(-2, 2, lp.num_variables)
+        y = rng.uniform(-2, 2, lp.num_constraints)
+        kx = s.spmv(abi.OP_K_SCALED, x)
+        kty = s.spmv(abi.OP_KT_SCALED, y)
+    Ks = CsrMatrix(K.num_rows, K.num_cols, K.row_offsets, K.col_indices,
+                   K.values * (np.repeat(d1, lens) * d2[K.col_indices]))  # v *= dr * dc, scaling.hpp:150-152
+    assert np.array_equal(kx, O.spmv(Ks, x))
+    assert np.array_equal(kty, O.spmv_transpose(Ks, y))
+
+
 @pytest.mark.parametrize("which", ["C1", "transport", "skewed"])
 def test_column_panels_match_oracle(which, monkeypatch):
     monkeypatch.setenv("PDLP_PANELS", "1")

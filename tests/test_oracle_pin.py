@@ -217,3 +217,23 @@ def test_golden_manifest_is_complete():
                 ("assign22", "blend", "degen", "diet", "freevars", "knaprelax", "pathflow", "prodmix",
                  "transport23", "twovar")]) >= 20  # acceptance needs >= 20 suite instances
     assert json.loads((GOLDEN / "ref_c1.json").read_text())["nnz"] == 100000
+
+
+def test_oracle_c2_first_100_iterates_match_reference_goldens():
+    """The C restatement re-drives C2 (BASELINE configs[1], 2M nonzeros)
+    exactly like the reference (tests/golden/make_golden_configs.py ran
+    oracle/_ref): counters, step sizes, primal weight and the sampled iterate
+    entries are bitwise equal over the first 100 iterations."""
+    meta = json.loads((GOLDEN / "configs.json").read_text())["C2"]
+    g = dict(np.load(GOLDEN / "configs_C2.npz"))
+    lp = generators.config("C2")
+    assert lp_hash(lp) == meta["instance_sha256"]
+    s = O.Session(lp, SolverParams(), "oracle")
+    for k in range(meta["iterates"]):
+        s.run(1)
+        it = s.iterate()
+        for key in ("total", "inner", "trials", "eta", "eta_hat", "omega"):
+            assert it[key] == g[key][k], (key, k)
+        assert np.array_equal(it["x"][g["ix"]], g["x_s"][k]) and np.array_equal(it["y"][g["iy"]], g["y_s"][k]), k
+        assert np.linalg.norm(it["x"]) == g["x_norm"][k] and np.linalg.norm(it["y"]) == g["y_norm"][k]
+    s.close()
