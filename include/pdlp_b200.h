@@ -87,8 +87,8 @@ enum {
 enum {
   /* GRAPH (STREAM if use_cuda_graph == 0) */
   PDLP_ENGINE_AUTO = 0,
-  /* one cooperative persistent kernel per evaluation window: TMA-fed tile
-   * pipeline, grid barriers, on-device step decisions (fast mode only) */
+  /* reserved: a removed persistent window engine (measured 2x slower than
+   * GRAPH); rejected with PDLP_EINVAL */
   PDLP_ENGINE_PERSISTENT = 1,
   /* CUDA graph: WHILE(conditional node) { dual kernel; primal kernel } */
   PDLP_ENGINE_GRAPH = 2,

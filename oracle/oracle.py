@@ -80,6 +80,15 @@ def load(kind: str = "oracle") -> C.CDLL:
     return lib
 
 
+def set_sum_order(order: int) -> None:
+    """Summation-order probe of the C restatement (0: the reference's
+    sequential step-size sums; 1: pairwise trees). Process-wide."""
+    lib = load("oracle")
+    lib.oracle_set_sum_order.argtypes = [C.c_int]
+    lib.oracle_set_sum_order.restype = None
+    lib.oracle_set_sum_order(int(order))
+
+
 def _f(lib, kind, name):
     return getattr(lib, PREFIX[kind] + name)
 

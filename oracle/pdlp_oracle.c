@@ -30,6 +30,24 @@ static int fail(int code, const char* fmt, ...) {
 
 const char* oracle_last_error(void) { return g_err; }
 
+/* Summation-order probe (tests only, default 0 = the reference's sequential
+ * loops). 1: the step-size sums dx^2, dy^2 and the interaction of
+ * adaptive_step_cached (solver.hpp:422-435) as pairwise trees over blocks of 8
+ * terms, i.e. another legal summation order of the same terms. It measures how
+ * far a reordering alone moves the reference's own iterates. */
+static int g_sum_order = 0;
+void oracle_set_sum_order(int order) { g_sum_order = order; }
+
+static double pairwise(const double* t, int64_t n) {
+  if (n <= 8) {
+    double a = 0.0;
+    for (int64_t i = 0; i < n; ++i) a += t[i];
+    return a;
+  }
+  const int64_t h = n / 2;
+  return pairwise(t, h) + pairwise(t + h, n - h);
+}
+
 /* std::min / std::max / std::clamp exactly as libstdc++ defines them. */
 static inline double smin(double a, double b) { return (b < a) ? b : a; }
 static inline double smax(double a, double b) { return (a < b) ? b : a; }
@@ -887,15 +905,26 @@ static step_out_t adaptive_step(oracle_session* s, int64_t k, double* kty_next) 
         return r;
       }
     double dx = 0.0;
-    for (int64_t i = 0; i < n; ++i) {
-      const double d = s->xn[i] - s->x[i];
-      dx += d * d;
-    }
     double dy = 0.0, inter = 0.0;
-    for (int64_t i = 0; i < m; ++i) {
-      const double d = s->yn[i] - s->y[i];
-      dy += d * d;
-      inter += d * (s->kxn[i] - s->kx[i]);
+    if (g_sum_order == 1) {
+      double* t = (double*)xmalloc((size_t)(n > m ? n : m) * sizeof(double));
+      for (int64_t i = 0; i < n; ++i) t[i] = (s->xn[i] - s->x[i]) * (s->xn[i] - s->x[i]);
+      dx = pairwise(t, n);
+      for (int64_t i = 0; i < m; ++i) t[i] = (s->yn[i] - s->y[i]) * (s->yn[i] - s->y[i]);
+      dy = pairwise(t, m);
+      for (int64_t i = 0; i < m; ++i) t[i] = (s->yn[i] - s->y[i]) * (s->kxn[i] - s->kx[i]);
+      inter = pairwise(t, m);
+      free(t);
+    } else {
+      for (int64_t i = 0; i < n; ++i) {
+        const double d = s->xn[i] - s->x[i];
+        dx += d * d;
+      }
+      for (int64_t i = 0; i < m; ++i) {
+        const double d = s->yn[i] - s->y[i];
+        dy += d * d;
+        inter += d * (s->kxn[i] - s->kx[i]);
+      }
     }
     const double mov = s->omega * dx + dy / s->omega;
     const double ia = fabs(inter);

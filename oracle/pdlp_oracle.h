@@ -65,6 +65,10 @@ int oracle_check_termination(const pdlp_lp* lp, const double* x, const double* y
 
 const char* oracle_last_error(void);
 
+/* Summation-order probe: 0 (default) the reference's sequential step-size
+ * sums, 1 pairwise trees (process-wide; tests only). */
+void oracle_set_sum_order(int order);
+
 #ifdef __cplusplus
 }
 #endif

@@ -33,8 +33,7 @@ constexpr int kVecPad = 8;           // index/value arrays padded for 128-bit ta
 
 // Tile geometry per kernel family (tiles.h). The iteration kernels take fat
 // tiles (16 nnz per thread) so C2-sized operators run in about one wave; the
-// persistent window kernel stages whole tiles in shared memory; the evaluation
-// kernels gather 4 values per nonzero and keep their staging small.
+// evaluation kernels gather 4 values per nonzero and keep their staging small.
 struct TileGeom {
   int stream_nnz;  // nnz per STREAM tile (staged products in shared memory)
   int stream_rows; // rows per STREAM tile = rows_per_thread * kThreads
@@ -45,11 +44,7 @@ struct TileGeom {
 #define PDLP_ITER_ROWS 1024
 #endif
 constexpr TileGeom kIterGeom{4096, PDLP_ITER_ROWS, 16, 4096};
-constexpr TileGeom kWinGeom{2048, 1024, 8, 2048};
 constexpr TileGeom kEvalGeom{1024, 1024, 8, 2048};
-// column-panel passes: stacked rows hold ~nnz/row/panels entries, so tiles take
-// up to 4096 rows (16 per thread) to keep ~4k nonzeros per CTA
-constexpr TileGeom kPanelGeom{4096, 4096, 16, 4096};
 constexpr int kStreamNnz = 4096;     // largest STREAM tile of any geometry
 constexpr int kStreamRows = 2048;
 

@@ -39,7 +39,7 @@ struct DevState {
   double eta_acc, eta_bar, eta_next, mov, inter;  // last accepted step
   unsigned ctr_dual;
   unsigned ctr_eval;
-  int32_t window_cont;  // set by the window kernel's decision: run another trial
+  int32_t window_cont;  // unused (layout)
   int32_t pad2;
   // ---- window chaining (graph engine, fast mode; chain_decide_kernel) ----
   double kkt_epoch_start;  // the host's restart-test values, mirrored for the device

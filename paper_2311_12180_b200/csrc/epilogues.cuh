@@ -1,6 +1,6 @@
 // epilogues.cuh — the fused projected updates of the two iteration SpMVs,
-// shared by the per-trial kernels (kernels.cu) and the persistent window
-// kernel (window.cu).
+// shared by the per-trial kernels (kernels.cu) and the column-panel sweeps
+// (panels.cu).
 #pragma once
 
 #include "common.cuh"
@@ -33,9 +33,8 @@ __device__ __forceinline__ double lambda_term(double lam, double l, double u) {
 
 
 // Loads of iteration vectors: the per-trial kernels may use the read-only
-// (.nc) path; the persistent window kernel reads data other CTAs wrote earlier
-// in the same launch, so it uses coherent L1-cached loads (kCoh), made fresh by
-// the gpu-scope fence at every grid barrier.
+// (.nc) path; kCoh selects coherent L1-cached loads for data other CTAs wrote
+// earlier in the same launch.
 template <bool kCoh>
 __device__ __forceinline__ double ldv(const double* p) {
   if (kCoh) return __ldca(p);

@@ -19,11 +19,11 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #include <limits>
 
 #include "kernels.cuh"
 #include "solver.cuh"
-#include "window.cuh"
 
 namespace pdlp {
 
@@ -53,8 +53,9 @@ void validate_params(const pdlp_params& p) {  // SolverParams::validate, solver.
     invalid("params: plan_world must equal world_size on a sharded rank");
   if (p.world_size > 1 && p.mode == PDLP_MODE_PARITY)
     invalid("params: parity mode runs on one device (world_size 1)");
-  if (p.world_size > 1 && p.engine == PDLP_ENGINE_PERSISTENT)
-    invalid("params: the persistent engine runs on one device (world_size 1)");
+  if (p.engine == PDLP_ENGINE_PERSISTENT)
+    invalid("params: the persistent window engine was removed (it measured 2x slower than the graph engine "
+            "on C1-C3); use PDLP_ENGINE_GRAPH or PDLP_ENGINE_STREAM");
 }
 
 }  // namespace
@@ -202,7 +203,7 @@ void Solver::setup(const pdlp_lp& lp) {
 
   cudaStream_t s = stream_;
   // ---- K = vstack(G, A) (sparse_matrix.hpp:181-200) in HBM, int32 indices ----
-  k_rp_.alloc(m_ + 1 + kVecPad);  // padded: the window kernel copies quad-aligned spans
+  k_rp_.alloc(m_ + 1 + kVecPad);  // padded for quad-aligned span loads
   k_rp_.zero(s);
   k_col_.alloc(nnz_ + kVecPad);
   k_val_orig_.alloc(nnz_ + kVecPad);
@@ -295,8 +296,8 @@ void Solver::setup(const pdlp_lp& lp) {
   }
   const int64_t r0 = k_cuts_[rank_], r1 = k_cuts_[rank_ + 1];
   const int64_t c0 = world_ > 1 ? kt_cuts_[rank_] : 0, c1 = world_ > 1 ? kt_cuts_[rank_ + 1] : n_;
-  // three tilings of each operator: iteration kernels, persistent window
-  // kernel, evaluation kernels (common.cuh TileGeom)
+  // two tilings of each operator: iteration kernels and evaluation kernels
+  // (common.cuh TileGeom)
   mark("offsets");
   // rows with mostly consecutive columns get element-interleaved lane groups
   std::vector<uint8_t> kcon, ktcon;
@@ -319,10 +320,6 @@ void Solver::setup(const pdlp_lp& lp) {
   }
   build_plan(k_it_, K_, rp_h, kIterGeom, kbrk, r0, r1, kc_p);
   build_plan(kt_it_, KT_, rpt_h, kIterGeom, ktbrk, c0, c1, ktc_p);
-  if (params_.engine == PDLP_ENGINE_PERSISTENT) {  // only the window kernel uses these
-    build_plan(k_win_, K_, rp_h, kWinGeom, {}, 0, m_);
-    build_plan(kt_win_, KT_, rpt_h, kWinGeom, {}, 0, n_);
-  }
   build_plan(k_ev_, K_, rp_h, kEvalGeom, kbrk, r0, r1, kc_p);
   build_plan(kt_ev_, KT_, rpt_h, kEvalGeom, ktbrk, c0, c1, ktc_p);
   if (trace) {
@@ -780,8 +777,8 @@ void Solver::allocate_iteration() {
   if (engine_ == PDLP_ENGINE_AUTO)
     engine_ = params_.use_cuda_graph ? PDLP_ENGINE_GRAPH : PDLP_ENGINE_STREAM;
   // fast per-trial kernels skip storing K'y' on accepted steps (8n bytes per
-  // iteration); the persistent window kernel keeps its own cache
-  it.kty_lazy = (!parity() && engine_ != PDLP_ENGINE_PERSISTENT && !std::getenv("PDLP_NO_LAZY_KTY")) ? 1 : 0;
+  // iteration)
+  it.kty_lazy = (!parity() && !std::getenv("PDLP_NO_LAZY_KTY")) ? 1 : 0;
   // L2 prefetch of the tiles before griddepcontrol.wait (overlapping the
   // previous kernel's tail) pays where the operators are mid-sized and mostly
   // L2-resident: C2 123.9 -> 119.3 ms per solve. Tiny operators only pay the
@@ -789,32 +786,6 @@ void Solver::allocate_iteration() {
   // gathered vector to the prefetched lines (C3 200.5 -> 207.4 ms).
   it.prefetch = (nnz_ >= (int64_t(1) << 20) && nnz_ <= (int64_t(8) << 20)) ? 1 : 0;
   if (const char* e = std::getenv("PDLP_PREFETCH")) it.prefetch = std::atoi(e) != 0;
-  if (engine_ == PDLP_ENGINE_PERSISTENT && parity())
-    invalid("params: the persistent engine runs fast mode only");
-  if (engine_ == PDLP_ENGINE_PERSISTENT) {
-    win_grid_ = window_grid(params_.device);
-    wd_part_.alloc(size_t(win_grid_) * 3);
-    wp_part_.alloc(size_t(win_grid_) * 2);
-    bar_.alloc(1);
-    bar_.zero(s);
-    wb_.wd_part = wd_part_.get();
-    wb_.wp_part = wp_part_.get();
-    wb_.bar = bar_.get();
-    auto split_list = [&](const OpPlan& p, DevBuf<int>& buf, const int*& ptr, int& count) {
-      std::vector<int> idx;
-      for (size_t i = 0; i < p.plan.tiles.size(); ++i) {
-        const Tile& t = p.plan.tiles[i];
-        if (t.kind == kTileChunk && t.nparts > 1 && t.part == 0) idx.push_back(int(i));
-      }
-      buf.alloc(std::max<size_t>(1, idx.size()));
-      if (!idx.empty())
-        PDLP_CUDA(cudaMemcpyAsync(buf.get(), idx.data(), idx.size() * sizeof(int), cudaMemcpyHostToDevice, s));
-      ptr = buf.get();
-      count = int(idx.size());
-    };
-    split_list(k_win_, k_split_, wb_.k_split, wb_.k_nsplit);
-    split_list(kt_win_, kt_split_, wb_.kt_split, wb_.kt_nsplit);
-  }
   it.st = state_dev_;
 
   X4_.alloc(size_t(n_) * 4);
@@ -1105,7 +1076,6 @@ void Solver::iterate_begin(int32_t* status) {
     primal_step(kPRetry);
     phase();
     ++launches_;
-    p_from_window_ = false;
   }
   if (status) *status = finished_ ? info_.status : PDLP_STATUS_RUNNING;
 }
@@ -1188,16 +1158,7 @@ void Solver::run_window(int target) {
                             cudaMemcpyHostToDevice, stream_));
   eval_fresh_ = false;
   PDLP_CUDA(cudaEventRecord(ev_w0_, stream_));
-  if (engine_ == PDLP_ENGINE_PERSISTENT) {
-    WinBufs wb = wb_;
-    wb.p_src = p_from_window_ ? wb_.wp_part
-                              : it_.p_part + size_t(st.trials_total & 1) * it_.p_tiles * 2;
-    wb.p_src_count = p_from_window_ ? win_grid_ : it_.p_tiles;
-    wb.p_src_window = p_from_window_ ? 1 : 0;
-    launch_window(k_win_.csr, kt_win_.csr, it_, wb, win_grid_, stream_);
-    p_from_window_ = true;
-    launches_ += 1;
-  } else if (engine_ == PDLP_ENGINE_GRAPH) {
+  if (engine_ == PDLP_ENGINE_GRAPH) {
     if (!graph_exec_) capture_window_graph();
     PDLP_CUDA(cudaGraphLaunch(graph_exec_, stream_));
   } else {
@@ -1240,8 +1201,7 @@ void Solver::run_window(int target) {
     eval_seconds_ += 1e-3 * double(ems);
     if (target == int(params_.evaluation_frequency)) window_time_est_ = 1e-3 * double(ms + ems);
   }
-  if (engine_ != PDLP_ENGINE_PERSISTENT)
-    launches_ += (it_.decide_sep == 1 ? 3 : 2) * (st.trials_total - trials_before);
+  launches_ += (it_.decide_sep == 1 ? 3 : 2) * (st.trials_total - trials_before);
   if (st.record_log && st.window_accepts > 0)
     step_log_.insert(step_log_.end(), log_host_.get(), log_host_.get() + st.window_accepts);
 }
@@ -1351,7 +1311,6 @@ void Solver::evaluation_block() {
   phase();
   launches_ += 3;
   eval_fresh_ = false;
-  p_from_window_ = false;
   ev.omega_after = st.omega;
   restart_log_.push_back(ev);
   kkt_epoch_start_ = rc.weighted(st.omega);
@@ -1806,7 +1765,7 @@ void Solver::import_shards(const ShardBlob* blobs, int world) {
   }
   shv_ = v;
   shard_view_upload();
-  linked_ = true;  // in-kernel flag barriers order the ranks (any engine but persistent)
+  linked_ = true;  // in-kernel flag barriers order the ranks
 }
 
 void Solver::shard_info(int64_t* out) const {

@@ -16,7 +16,6 @@
 #include "device_state.h"
 #include "kernels.cuh"
 #include "tiles.h"
-#include "window.cuh"
 
 namespace pdlp {
 
@@ -268,7 +267,7 @@ class Solver {
   // operator storage: K = (G; A) and its separately stored transpose
   DevBuf<int> k_rp_, k_col_, kt_rp_, kt_col_;
   DevBuf<double> k_val_, k_val_orig_, kt_val_, kt_val_orig_;
-  OpPlan k_it_, kt_it_, k_win_, kt_win_, k_ev_, kt_ev_;
+  OpPlan k_it_, kt_it_, k_ev_, kt_ev_;
   PanelOp kpan_, ktpan_;
   DevCsr K_{}, KT_{};  // the iteration-kernel tilings (this rank's tiles)
   DevCsr K_full_{}, KT_full_{};  // every tile (kernel-level API on a sharded rank)
@@ -318,15 +317,8 @@ class Solver {
   double window_seconds_ = 0.0, eval_seconds_ = 0.0;
   cudaEvent_t ev_e1_ = nullptr;
   EvalFork fork_{};  // side stream for the concurrent evaluation passes
-  // persistent window engine
-  int engine_ = PDLP_ENGINE_PERSISTENT;
-  int win_grid_ = 0;
-  bool p_from_window_ = false;
+  int engine_ = PDLP_ENGINE_GRAPH;
   bool eval_fresh_ = false;  // EvalOut on the host matches the device state
-  DevBuf<double> wd_part_, wp_part_;
-  DevBuf<int> k_split_, kt_split_;  // split rows of the window plans (first-slice tiles)
-  DevBuf<GridBar> bar_;
-  WinBufs wb_{};
   std::vector<pdlp_step_log_entry> step_log_;
   std::vector<pdlp_restart_event> restart_log_;
   pdlp_result_info info_{};

@@ -14,6 +14,17 @@ configs.json:
     iterate);
   * C2 only: the reference's full solve at eps 1e-4 and 1e-8 (solve(),
     solver.hpp:935-940): status, iterations, restarts, objectives.
+
+    python tests/golden/make_golden_configs.py --reorder-drift [C2 C3 C4]
+
+adds `reorder_drift` to each entry: how far the reference's own first N
+iterates move when only the summation order of the step-size sums (dx^2, dy^2,
+interaction; solver.hpp:422-435) changes from sequential to pairwise trees.
+It is measured on the C restatement (oracle/, pinned bitwise to the
+reference), with the worst relative error over the N iterates in the 2-norm
+and max-norm, over z = (x, y), x and y, as tests/test_gpu_configs.py measures
+fast mode. This is the floor any order other than the reference's own
+sequential one can reach.
 """
 from __future__ import annotations
 
@@ -75,8 +86,61 @@ def iterates(name: str, lp) -> dict:
     return out
 
 
+def reorder_drift(name: str, lp) -> dict:
+    """The two runs go one after the other (C4's sessions take ~35 GB of host
+    memory each); the sequential run's iterates are parked on disk."""
+    import tempfile
+
+    N = ITERATES[name]
+    n, m = lp.num_variables, lp.num_constraints
+    with tempfile.TemporaryDirectory(dir="/root") as tmp:
+        store = np.lib.format.open_memmap(f"{tmp}/z.npy", mode="w+", dtype=np.float64, shape=(N, n + m))
+        counters = []
+        O.set_sum_order(0)
+        a = O.Session(lp, SolverParams(), "oracle")
+        for k in range(N):
+            a.run(1)
+            ia = a.iterate()
+            store[k, :n], store[k, n:] = ia["x"], ia["y"]
+            counters.append((ia["total"], ia["trials"]))
+        a.close()
+        del a
+        w2 = wi = 0.0
+        O.set_sum_order(1)
+        try:
+            b = O.Session(lp, SolverParams(), "oracle")
+            for k in range(N):
+                b.run(1)
+                ib = b.iterate()
+                assert (ib["total"], ib["trials"]) == counters[k]
+                za = np.asarray(store[k])
+                zb = np.concatenate([ib["x"], ib["y"]])
+                for u, v in ((za, zb), (za[:n], ib["x"]), (za[n:], ib["y"])):
+                    w2 = max(w2, float(np.linalg.norm(v - u) / max(np.linalg.norm(u), 1e-300)))
+                    wi = max(wi, float(np.abs(v - u).max(initial=0.0) / max(np.abs(u).max(initial=0.0), 1e-300)))
+            b.close()
+        finally:
+            O.set_sum_order(0)
+        del store
+    return {"rel2": w2, "relinf": wi, "iterates": N, "order": "pairwise step-size sums (oracle, sum order 1)"}
+
+
 def main() -> None:
-    names = sys.argv[1:] or ["C2", "C3", "C4"]
+    args = sys.argv[1:]
+    if args and args[0] == "--reorder-drift":
+        names = args[1:] or ["C2", "C3", "C4"]
+        meta_path = OUT / "configs.json"
+        meta = json.loads(meta_path.read_text())
+        for name in names:
+            t = time.time()
+            lp = generators.config(name)
+            assert lp_hash(lp) == meta[name]["instance_sha256"]
+            meta[name]["reorder_drift"] = reorder_drift(name, lp)
+            print(f"{name}: {meta[name]['reorder_drift']} ({time.time() - t:.0f} s)", flush=True)
+            meta_path.write_text(json.dumps(meta, indent=1, sort_keys=True) + "\n")
+            del lp
+        return
+    names = args or ["C2", "C3", "C4"]
     meta_path = OUT / "configs.json"
     meta = json.loads(meta_path.read_text()) if meta_path.exists() else {}
     for name in names:

@@ -237,3 +237,20 @@ def test_oracle_c2_first_100_iterates_match_reference_goldens():
         assert np.array_equal(it["x"][g["ix"]], g["x_s"][k]) and np.array_equal(it["y"][g["iy"]], g["y_s"][k]), k
         assert np.linalg.norm(it["x"]) == g["x_norm"][k] and np.linalg.norm(it["y"]) == g["y_norm"][k]
     s.close()
+
+
+def test_c2_reorder_drift_matches_committed_floor():
+    """configs.json `reorder_drift` (the floor of tests/test_gpu_configs.py's
+    fast-mode bars) is reproducible: the C restatement re-run with pairwise
+    step-size sums (oracle sum order 1) against its sequential self gives the
+    committed C2 figures exactly, and a reordering alone already moves the
+    reference's iterates."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("mgc", GOLDEN / "make_golden_configs.py")
+    mgc = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mgc)
+    meta = json.loads((GOLDEN / "configs.json").read_text())["C2"]
+    got = mgc.reorder_drift("C2", generators.config("C2"))
+    assert got["rel2"] == meta["reorder_drift"]["rel2"] and got["relinf"] == meta["reorder_drift"]["relinf"]
+    assert got["rel2"] > 0.0

@@ -52,7 +52,7 @@ def test_invalid_shard_params_are_einval_without_gpu():
     lib = load_library()
     lp = generators.small_random_lp(6, 3, 2, seed=1)
     for kw in (dict(world_size=2, rank=2), dict(world_size=9), dict(world_size=2, mode=1),
-               dict(world_size=2, engine=abi.ENGINE_PERSISTENT)):
+               dict(world_size=2, engine=abi.ENGINE_PERSISTENT), dict(engine=abi.ENGINE_PERSISTENT)):
         h = C.c_void_p()
         lpa, pa = lp.to_abi(), SolverParams(**kw).to_abi()
         assert lib.pdlp_create(C.byref(lpa), C.byref(pa), C.byref(h)) == abi.PDLP_EINVAL, kw
