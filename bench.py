@@ -15,8 +15,14 @@ the K timed solves (CUDA events on the solver's stream, inside libpdlp_b200).
 (H2D of the 2.4 GB instance, K^T build, preconditioning, panel plans) +
 pdlp_solve + pdlp_get_solution (D2H of x, y, lambda) every step. The inputs
 (> 4 GB) exceed the 126 MB L2; L2 is also flushed between timed solves.
-N > 1: every rank solves its own replica on its own GPU (weak scaling, no
-collective on the data path).
+N > 1 (torchrun, one process per GPU, device = LOCAL_RANK): ONE row-sharded
+solve of the instance (ShardRank: K and K^T cut by rows into N contiguous
+ranges, each rank computing its rows of y' / Kx' and its columns of x' / K'y'
+and pushing them into the peers' buffers inside the kernels, csrc/shard.cuh);
+`value` = iterations of the instance / max-over-ranks device time ("scaling":
+"strong"). --replicas runs N independent solves instead (weak scaling), which
+is also the fallback, reported in `config.parallelism`, if the sharded setup
+fails.
 
 --impl reference times the reference CPU solver (oracle/_ref: the unmodified
 pdhglp headers compiled in place) on the host cores: one shared setup of the
@@ -284,14 +290,17 @@ def run_ours(args):
 
     rank, world, local = env_rank()
     dist = None
+    device = 0
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
-    device = local if world > 1 else 0
+        ndev = max(1, torch.cuda.device_count())
+        device = local % ndev
+        torch.cuda.set_device(device)
+        # several ranks per GPU (tests on a one-GPU box): NCCL refuses shared devices
+        dist.init_process_group("nccl" if world <= ndev else "gloo")
     torch.cuda.set_device(device)
-    from paper_2311_12180_b200 import Solver, SolverParams, generators
+    from paper_2311_12180_b200 import ShardRank, Solver, SolverParams, generators
 
     # the CPU baseline runs beside the GPU timing in a child process pinned to
     # the last core (reference setup on C4 takes minutes of host time)
@@ -301,7 +310,7 @@ def run_ours(args):
                                      "--cpu-iters", str(args.cpu_iters)], stdout=subprocess.PIPE,
                                     stderr=subprocess.PIPE, text=True)
     t = time.perf_counter()
-    lp = generators.config(CONFIG)
+    lp = generators.config(args.config)
     gen_s = time.perf_counter() - t
     n, m, nnz = lp.num_variables, lp.num_constraints, lp.nnz
     params = SolverParams(eps_optimal=1e-4, device=device)
@@ -312,8 +321,37 @@ def run_ours(args):
         if dist:
             dist.barrier()
 
+    def allmax(v: float) -> float:
+        if not dist:
+            return float(v)
+        on = f"cuda:{device}" if dist.get_backend() == "nccl" else "cpu"
+        t_ = torch.tensor([float(v)], dtype=torch.float64, device=on)
+        dist.all_reduce(t_, op=dist.ReduceOp.MAX)
+        return float(t_.item())
+
+    # N > 1: one row-sharded solve of the instance over all ranks (
+    # each rank one GPU, x' / y' pushed to peers inside the kernels); replicas
+    # (one independent solve per GPU) only if the sharded setup fails
+    sharded = world > 1 and not args.replicas
+    fallback = None
+
+    def make():
+        return ShardRank(lp, params, device=device) if sharded else Solver(lp, params)
+
     t = time.perf_counter()
-    solver = Solver(lp, params)
+    solver, err = None, ""
+    try:
+        solver = make()
+    except Exception as e:  # noqa: BLE001 - reported in the JSON line
+        err = f"{type(e).__name__}: {e}"
+    if sharded and allmax(1.0 if solver is None else 0.0) > 0.0:
+        if solver is not None:
+            solver.close()
+        fallback = (err or "a peer rank failed")[:300]
+        sharded = False
+        solver = make()
+    elif solver is None:
+        raise RuntimeError(err)
     setup_s = time.perf_counter() - t
     for _ in range(args.warmup):
         solver.solve()
@@ -337,27 +375,25 @@ def run_ours(args):
     barrier()
     wall = time.perf_counter() - wall0
     clk = clocks.stop()
-    t = torch.tensor([dev_s], dtype=torch.float64, device=f"cuda:{device}")
-    it_t = torch.tensor([float(iters)], dtype=torch.float64, device=f"cuda:{device}")
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(it_t, op=dist.ReduceOp.SUM)
-    max_dev_s, total_iters = float(t.item()), float(it_t.item())
+    max_dev_s = allmax(dev_s)
+    # sharded: every rank runs the same iterations of the one instance; replicas: every rank its own
+    total_iters = float(iters) if sharded or not dist else float(iters) * world
     value = total_iters / max_dev_s
     last = results[-1]
 
-    # ---- roofline of the dominant kernel group (dual: K x' + update; primal: K'y' + update) ----
+    # ---- roofline of the dominant kernel group (dual: K x' + update; primal: K'y' + update), one GPU ----
     peak, peak_kind = peaks()
-    kern = {}
-    for which, name in ((0, "dual"), (1, "primal"), (2, "spmv_K"), (3, "spmv_KT")):
-        ms, alg = solver.time_kernel(which, 20)
-        kb = solver.kernel_bytes(which)
-        kern[name] = {"us": 1e3 * ms, "alg_bytes": alg, "moved_bytes": kb["moved"], "panels": kb["panels"],
-                      "alg_gbs": alg / (ms * 1e-3) / 1e9, "moved_gbs": kb["moved"] / (ms * 1e-3) / 1e9}
+    kern, dk, dom, traffic = {}, None, None, {}
+    if world == 1:
+        for which, name in ((0, "dual"), (1, "primal"), (2, "spmv_K"), (3, "spmv_KT")):
+            ms, alg = solver.time_kernel(which, 20)
+            kb = solver.kernel_bytes(which)
+            kern[name] = {"us": 1e3 * ms, "alg_bytes": alg, "moved_bytes": kb["moved"], "panels": kb["panels"],
+                          "alg_gbs": alg / (ms * 1e-3) / 1e9, "moved_gbs": kb["moved"] / (ms * 1e-3) / 1e9}
+        dom = "primal" if kern["primal"]["us"] >= kern["dual"]["us"] else "dual"
+        dk = kern[dom]
+        traffic = profile_traffic(CONFIG).get(dom, {})
     solver.close()
-    dom = "primal" if kern["primal"]["us"] >= kern["dual"]["us"] else "dual"
-    dk = kern[dom]
-    traffic = profile_traffic(CONFIG).get(dom, {})
 
     # ---- e2e through the C-ABI with host buffers ----
     e2e_steps = max(1, min(args.steps, E2E_STEPS))
@@ -369,7 +405,7 @@ def run_ours(args):
         flush.fill_(1.0)
         barrier()
         t0 = time.perf_counter()
-        s2 = Solver(lp, params)  # pdlp_create: H2D + K^T + preconditioning + plans
+        s2 = make()  # pdlp_create (+ the shard link): H2D + K^T + preconditioning + plans
         t1 = time.perf_counter()
         r2 = s2.solve()  # pdlp_solve + pdlp_get_solution (D2H)
         t2 = time.perf_counter()
@@ -381,15 +417,11 @@ def run_ours(args):
         parts["solve_ms"] += 1e3 * (t2 - t1) / e2e_steps
         parts["destroy_ms"] += 1e3 * (t3 - t2) / e2e_steps
         e2e_iters += r2.iterations
-    et = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{device}")
-    ei = torch.tensor([float(e2e_iters)], dtype=torch.float64, device=f"cuda:{device}")
-    if dist:
-        dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        dist.all_reduce(ei, op=dist.ReduceOp.SUM)
-    e2e_value = float(ei.item()) / float(et.item())
+    e2e_total = float(e2e_iters) if sharded or not dist else float(e2e_iters) * world
+    e2e_value = e2e_total / allmax(e2e_s)
     del lp
 
-    c2 = c2_extra(device) if rank == 0 and not args.no_c2 else None
+    c2 = c2_extra(device) if rank == 0 and world == 1 and not args.no_c2 else None
 
     cpu = None
     if cpu_proc is not None:
@@ -401,25 +433,22 @@ def run_ours(args):
                    "sample": f"failed: {err.strip()[-300:]}"}
 
     if rank == 0:
+        if world == 1:
+            par = "single GPU"
+        elif sharded:
+            par = f"row-sharded x{world} (one instance; x', y' pushed to peers inside the kernels, csrc/shard.cuh)"
+        else:
+            par = f"replicas x{world}" + (f" (sharded setup failed: {fallback})" if fallback else "")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * max_dev_s / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, no dataset)",
-            "config": {"workload": WORKLOAD, "eps": 1e-4, "seed": generators.SEEDS[CONFIG],
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator, no dataset)",
+            "config": {"workload": WORKLOAD if args.config == CONFIG else args.config, "eps": 1e-4,
+                       "seed": generators.SEEDS[args.config], "parallelism": par,
                        "l2": "inputs (>4 GB) exceed L2; also flushed between timed solves (256 MiB write)"},
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "steps": e2e_steps, "per_step": parts},
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": dk["alg_gbs"], "peak": peak, "unit": "GB/s",
-                         "frac": dk["alg_gbs"] / peak, "traffic": traffic.get("dram_bytes_per_launch"),
-                         "peak_source": peak_kind, "bytes_per_launch": dk["alg_bytes"],
-                         "moved_bytes_per_launch": dk["moved_bytes"], "moved_frac": dk["moved_gbs"] / peak,
-                         "launch_us": dk["us"], "panels": dk["panels"],
-                         "traffic_source": traffic.get("source")},
-            "iteration_roofline": {"b_iter_bytes": b_iter(n, m, nnz),
-                                   "achieved_gbs": b_iter(n, m, nnz) * value / world / 1e9,
-                                   "frac": b_iter(n, m, nnz) * value / world / 1e9 / peak},
-            "kernels": kern,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d * (world if sharded else 1),
+                    "d2h_bytes_per_step": d2h * (world if sharded else 1), "steps": e2e_steps, "per_step": parts},
             "time_to_tolerance_ms": 1e3 * last.info["device_seconds"], "iterations": last.iterations,
             "window_ms": 1e3 * last.info["window_seconds"], "eval_ms": 1e3 * last.info["eval_seconds"],
             "windows_chained": last.info["eval_seconds"] == 0.0,
@@ -430,6 +459,21 @@ def run_ours(args):
             "setup_ms": 1e3 * last.info["setup_seconds"], "create_s": setup_s, "generate_s": gen_s,
             "gpu_launches": int(launches), "clocks": clk, "wall_s": wall,
         }
+        if dk is not None:
+            line["roofline"] = {"bound": "hbm", "kernel": dom, "achieved": dk["alg_gbs"], "peak": peak, "unit": "GB/s",
+                                "frac": dk["alg_gbs"] / peak, "traffic": traffic.get("dram_bytes_per_launch"),
+                                "peak_source": peak_kind, "bytes_per_launch": dk["alg_bytes"],
+                                "moved_bytes_per_launch": dk["moved_bytes"], "moved_frac": dk["moved_gbs"] / peak,
+                                "launch_us": dk["us"], "panels": dk["panels"],
+                                "traffic_source": traffic.get("source")}
+            line["iteration_roofline"] = {"b_iter_bytes": b_iter(n, m, nnz),
+                                          "achieved_gbs": b_iter(n, m, nnz) * value / 1e9,
+                                          "frac": b_iter(n, m, nnz) * value / 1e9 / peak}
+            line["kernels"] = kern
+        else:
+            line["iteration_roofline"] = {"b_iter_bytes": b_iter(n, m, nnz),
+                                          "achieved_gbs_per_gpu": b_iter(n, m, nnz) * value / world / 1e9,
+                                          "frac_per_gpu": b_iter(n, m, nnz) * value / world / 1e9 / peak}
         if c2:
             line["c2"] = c2
         if cpu:
@@ -449,6 +493,8 @@ def main():
     ap.add_argument("--ref-iters", type=int, default=1, help="reference arm: iterations per solve per step")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c2", action="store_true")
+    ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of one sharded solve")
+    ap.add_argument("--config", default=CONFIG, help=argparse.SUPPRESS)  # tests: a smaller config
     ap.add_argument("--cpu-sample", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.cpu_sample:

@@ -15,8 +15,8 @@ from .lp import (
     SolverParams,
     SolveStatus,
 )
-from .api import (PdlpError, ShardGroup, Solver, load_library, parse_mps, plan_shards, read_mps, solve,
-                  solve_distributed, write_solution)
+from .api import (PdlpError, ShardGroup, ShardRank, Solver, device_count, load_library, parse_mps, plan_shards,
+                  read_mps, solve, solve_distributed, write_solution)
 
 __all__ = [
     "CsrMatrix",
@@ -38,6 +38,8 @@ __all__ = [
     "parse_mps",
     "write_solution",
     "ShardGroup",
+    "ShardRank",
+    "device_count",
     "plan_shards",
     "solve_distributed",
 ]

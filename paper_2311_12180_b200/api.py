@@ -308,25 +308,52 @@ class ShardGroup:
         self.close()
 
 
-def solve_distributed(lp: GeneralFormLp, params: SolverParams | None = None, group=None) -> SolveResult:
-    """One rank of a row-sharded solve, one process per GPU: rank / world from
-    torch.distributed (any backend; only the CUDA-IPC blobs travel over it),
-    then the ranks exchange data GPU-to-GPU inside the kernels."""
-    import dataclasses
+class ShardRank:
+    """One rank of a row-sharded solve, one process per GPU: the
+    rank and world come from torch.distributed (any backend; only the ~1 KB
+    CUDA-IPC blobs travel over it), the device from LOCAL_RANK (modulo the
+    visible devices, so a one-GPU box can host several ranks for tests).
+    After the blob exchange the ranks move data GPU-to-GPU inside the kernels
+    (csrc/shard.cuh). The handle stays linked for repeated solves."""
 
-    import torch.distributed as dist
+    def __init__(self, lp: GeneralFormLp, params: SolverParams | None = None, group=None, device=None):
+        import dataclasses
 
-    world, rank = dist.get_world_size(group), dist.get_rank(group)
-    base = params or SolverParams()
-    s = Solver(lp, dataclasses.replace(base, world_size=world, rank=rank))
-    try:
-        blobs: list = [None] * world
-        dist.all_gather_object(blobs, s.shard_export(), group=group)
-        s.shard_import(blobs)
-        dist.barrier(group)
-        return s.solve()
-    finally:
-        s.close()
+        import torch.distributed as dist
+
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        if device is None:
+            device = int(os.environ.get("LOCAL_RANK", rank)) % max(1, device_count())
+        base = params or SolverParams()
+        self.rank, self.world, self.device = rank, world, device
+        self.solver = Solver(lp, dataclasses.replace(base, world_size=world, rank=rank, device=device))
+        try:
+            blobs: list = [None] * world
+            dist.all_gather_object(blobs, self.solver.shard_export(), group=group)
+            self.solver.shard_import(blobs)
+            dist.barrier(group)
+        except BaseException:
+            self.solver.close()
+            raise
+
+    def solve(self) -> SolveResult:
+        return self.solver.solve()
+
+    def close(self) -> None:
+        self.solver.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def solve_distributed(lp: GeneralFormLp, params: SolverParams | None = None, group=None, device=None) -> SolveResult:
+    """One rank of a row-sharded solve, one process per GPU (ShardRank): every
+    rank returns the same result."""
+    with ShardRank(lp, params, group, device) as r:
+        return r.solve()
 
 
 MPS_FIXED, MPS_FREE, MPS_AUTO = 0, 1, 2
@@ -410,7 +437,7 @@ def solve(lp: GeneralFormLp, params: SolverParams | None = None) -> SolveResult:
         return s.solve()
 
 
-__all__ = ["Solver", "solve", "load_library", "default_params", "PdlpError", "library_path", "read_mps",
+__all__ = ["Solver", "ShardRank", "solve", "load_library", "default_params", "PdlpError", "library_path", "read_mps",
            "parse_mps", "write_solution", "MPS_FIXED", "MPS_FREE", "MPS_AUTO", "ShardGroup", "plan_shards",
            "csr_from_triplets",
            "solve_distributed"]

@@ -20,8 +20,15 @@
 // rows' running sums over them in entry order. The running sums live in `acc`
 // between passes (16 B per row per pass); the last pass applies the fused
 // update of the dual or primal kernel (DualEpi / PrimalEpi) instead, with one
-// reduction partial per block. (TMA bulk copies of the blocks, per CTA with a
-// 2-3 stage ring and per warp, were measured 1.7-2.3x slower on C4.)
+// reduction partial per block. Measured slower on C4 and not kept (DESIGN.md
+// §3): TMA bulk copies of the blocks (per CTA with a 2-3 stage ring, per warp;
+// 1.7-2.3x); row bands whose running sums stay L2-resident beside 16-32 MB
+// panels, as one launch per (band, panel) (K 2.3-3.6 ms vs 1.7), as a
+// persistent CTA or warp sweep with cp.async double buffering (3.4-6.9 ms);
+// 2048-row blocks (K 1.9-2.5 ms); an L2 prefetch of the block one wave ahead
+// (K 1.74-1.92 ms vs 1.70). The pass is latency-bound at 4 CTAs of 64
+// registers per SM (ncu: long-scoreboard 44% of stall samples, 48% warps
+// active, ~3.2 TB/s of DRAM traffic).
 //
 // Every row is summed by one thread, starting from 0.0, in increasing column
 // order: exactly the reference's `out[r] += val * x[col]` sequence. The panel
@@ -69,7 +76,10 @@ __device__ __forceinline__ void st_acc(double* p, double v) {
 
 using SweepOp = PanelView;
 
-constexpr int kSweepRows = kIterGeom.stream_rows;  // rows per CTA: 4 per thread, stride kThreads
+#ifndef PDLP_SWEEP_ROWS
+#define PDLP_SWEEP_ROWS 1024
+#endif
+constexpr int kSweepRows = PDLP_SWEEP_ROWS;  // rows per CTA: 4 or 8 per thread, stride kThreads
 constexpr int kSweepRPT = kSweepRows / kThreads;
 #ifndef PDLP_SWEEP_CHUNK
 #define PDLP_SWEEP_CHUNK 2048
@@ -80,7 +90,8 @@ constexpr int kSweepRPT = kSweepRows / kThreads;
 constexpr int kSweepChunk = PDLP_SWEEP_CHUNK;      // products staged per round (16 KB)
 constexpr int kSweepPer = kSweepChunk / kThreads;  // entries per thread per round, all in flight
 constexpr int kSweepCtasPerSm = PDLP_SWEEP_CTAS;
-static_assert(kSweepRows == 4 * kThreads, "four count bytes and four rows per thread");
+
+static_assert(kSweepRPT == 4 || kSweepRPT == 8, "four or eight count bytes and rows per thread");
 
 struct SweepSmem {
   int off[kSweepRows + 1];
@@ -205,7 +216,12 @@ __device__ __forceinline__ unsigned sweep_block(const SweepOp& op, int p, int b,
   // independent loads first: the block's entry range, its count bytes, the sums
   const int* bo = op.boff + size_t(p) * (op.nblk + 1) + b;
   const int e0 = __ldg(bo), e1 = __ldg(bo + 1);
-  const unsigned cw = ld_stream_u32_ef(op.cnt + size_t(p) * op.rows_pad + size_t(b) * kSweepRows + 4 * tid, ef);
+  uint2 cw;
+  {
+    const unsigned char* cp = op.cnt + size_t(p) * op.rows_pad + size_t(b) * kSweepRows + kSweepRPT * tid;
+    cw.x = ld_stream_u32_ef(cp, ef);
+    cw.y = kSweepRPT == 8 ? ld_stream_u32_ef(cp + 4, ef) : 0u;
+  }
   const int r0 = b * kSweepRows + tid;
 #pragma unroll
   for (int q = 0; q < kSweepRPT; ++q) acc[q] = p > 0 ? ld_acc(op.acc + r0 + q * kThreads) : 0.0;
@@ -233,27 +249,23 @@ __device__ __forceinline__ unsigned sweep_block(const SweepOp& op, int p, int b,
     }
   };
   stage(0, min(E, kSweepChunk));
-  // row offsets inside the block (4 rows' count bytes per thread, block scan)
-  int c[4], tot = 0;
+  // row offsets inside the block (the thread's rows' count bytes, block scan)
+  int tot = 0;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) c[i] = int((cw >> (8 * i)) & 255u), tot += c[i];
+  for (int i = 0; i < kSweepRPT; ++i) tot += int(((i < 4 ? cw.x : cw.y) >> (8 * (i & 3))) & 255u);
   int Et;
   const int ex = block_excl_scan(tot, sm.warp, &Et);  // (its barriers also publish the staged products)
-  sm.off[4 * tid] = ex;
-  sm.off[4 * tid + 1] = ex + c[0];
-  sm.off[4 * tid + 2] = ex + c[0] + c[1];
-  sm.off[4 * tid + 3] = ex + c[0] + c[1] + c[2];
+  {
+    int o = ex;
+#pragma unroll
+    for (int i = 0; i < kSweepRPT; ++i) {
+      sm.off[kSweepRPT * tid + i] = o;
+      o += int(((i < 4 ? cw.x : cw.y) >> (8 * (i & 3))) & 255u);
+    }
+  }
   if (tid == kThreads - 1) sm.off[kSweepRows] = Et;
   __syncthreads();
-  int o[kSweepRPT], e[kSweepRPT];
   unsigned has = 0;
-#pragma unroll
-  for (int q = 0; q < kSweepRPT; ++q) {
-    const int r = tid + q * kThreads;
-    o[q] = sm.off[r];
-    e[q] = sm.off[r + 1];
-    has |= (e[q] > o[q] ? 1u : 0u) << q;
-  }
   for (int c0 = 0; c0 < E; c0 += kSweepChunk) {
     const int c1 = min(E, c0 + kSweepChunk);
     if (c0 > 0) {  // a further round of an oversized block
@@ -263,7 +275,10 @@ __device__ __forceinline__ unsigned sweep_block(const SweepOp& op, int p, int b,
     }
 #pragma unroll
     for (int q = 0; q < kSweepRPT; ++q) {
-      const int k0 = max(o[q], c0), k1 = min(e[q], c1);
+      const int r = tid + q * kThreads;
+      const int o = sm.off[r], e = sm.off[r + 1];
+      if (c0 == 0) has |= (e > o ? 1u : 0u) << q;
+      const int k0 = max(o, c0), k1 = min(e, c1);
       for (int k = k0; k < k1; ++k) acc[q] = acc[q] + sm.prod[k - c0];  // sparse_matrix.hpp:128-130
     }
   }

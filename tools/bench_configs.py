@@ -21,7 +21,16 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 from paper_2311_12180_b200 import Solver, SolverParams, generators  # noqa: E402
 
-PEAK = 6650.0
+def _peak() -> float:
+    """HBM peak: MEASURED_PEAKS.json (driver-written) when present, else the
+    6650 GB/s fallback of B200_PROFILING.md -- the same choice as bench.py."""
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import bench
+
+    return bench.peaks()[0]
+
+
+PEAK = _peak()
 LIMITS = {"C1": 60.0, "C2": 120.0, "C3": 120.0, "C4": 120.0, "C5": 240.0}
 FIXED_ITERS = {"C1": 2048, "C2": 2048, "C3": 1024, "C4": 512, "C5": 256}
 
