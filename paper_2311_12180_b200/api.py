@@ -78,6 +78,7 @@ def load_library(build_if_missing: bool = True) -> C.CDLL:
         "pdlp_shard_export": (C.c_int, [H, C.c_void_p, C.c_int64]),
         "pdlp_shard_import": (C.c_int, [H, C.c_void_p, C.c_int32]),
         "pdlp_shard_info": (C.c_int, [H, i64p]),
+        "pdlp_shard_exchange": (C.c_int, [H, i64p]),
         "pdlp_plan_shards": (C.c_int, [C.POINTER(abi.PdlpLp), C.c_int32, i64p, i64p]),
     }
     for name, (res, args) in sig.items():
@@ -207,6 +208,13 @@ class Solver:
         keys = ("world", "rank", "row0", "row1", "col0", "col1", "k_tiles", "kt_tiles", "k_tiles_all",
                 "kt_tiles_all")
         return {k: int(v) for k, v in zip(keys, out)}
+
+    def shard_exchange(self) -> dict:
+        """Values this rank pushes to peers per trial: with the gather masks
+        and with an all-to-all push (pdlp_shard_exchange)."""
+        out = np.zeros(2, np.int64)
+        _check(self._lib.pdlp_shard_exchange(self._h, abi.i64ptr(out)))
+        return {"pushed": int(out[0]), "all_to_all": int(out[1])}
 
     def shard_export(self) -> bytes:
         size = int(self._lib.pdlp_shard_blob_size())

@@ -245,6 +245,15 @@ int pdlp_shard_info(pdlp_handle* h, int64_t* out) {
   return guarded([&] { h->solver->shard_info(out); });
 }
 
+int pdlp_shard_exchange(pdlp_handle* h, int64_t* out) {
+  if (!h) return null_handle();
+  if (!out) {
+    g_last_error = "null output";
+    return PDLP_EINVAL;
+  }
+  return guarded([&] { h->solver->shard_exchange(out); });
+}
+
 int pdlp_plan_shards(const pdlp_lp* lp, int32_t world, int64_t* k_cuts, int64_t* kt_cuts) {
   if (!lp || !k_cuts || !kt_cuts) {
     g_last_error = "null argument";

@@ -176,6 +176,10 @@ struct DevIter {
   int col0, col1;          // own rows of K^T = columns (x, K'y, avg_x slices)
   const ShardView* shv;    // peer table (device memory)
   ShardSync* sync;         // own sync block
+  // per value, the peers whose rows read it (bit q: rank q), so a trial pushes
+  // x' / y' only where it is gathered; nullptr: every peer
+  const unsigned* xmask;   // (n) ranks whose rows of K hold column j
+  const unsigned* ymask;   // (m) ranks whose rows of K^T (columns of K) hold row i
 };
 
 // Vectors of the evaluation block.

@@ -46,13 +46,39 @@ __device__ __forceinline__ double2 ldv2(const double* p) {
   return __ldg(reinterpret_cast<const double2*>(p));
 }
 
-// Peer copies of the values an epilogue owns (row sharding, shard.cuh).
+// Dense operand streams of rows_strided: default caching, or kStreamIO =
+// L2 evict-first style streaming (ld/st .cs) so a column-panel sweep's final
+// pass does not push its L2-resident panel slice out with the update streams.
+template <bool kCoh, bool kStreamIO>
+__device__ __forceinline__ double ld_io(const double* p) {
+  if (kStreamIO) return __ldcs(p);
+  return ldv<kCoh>(p);
+}
+template <bool kStreamIO>
+__device__ __forceinline__ double ld_io_plain(const double* p) {
+  if (kStreamIO) return __ldcs(p);
+  return *p;
+}
+template <bool kStreamIO>
+__device__ __forceinline__ void st_io(double* p, double v) {
+  if (kStreamIO)
+    __stcs(p, v);
+  else
+    *p = v;
+}
+
+// Peer copies of the values an epilogue owns (row sharding, shard.cuh): to
+// every peer, or only to the peers that gather value i (mask[i], bit q = rank q).
 struct PeerPush {
   double* const* field;  // ShardView pointer array of the exchanged buffer
   size_t off;            // element offset of the active rotation buffer
   int world, rank;
+  const unsigned* mask = nullptr;
   __device__ __forceinline__ void operator()(int i, double v) const {
-    push_peers(field, world, rank, off + size_t(i), v);
+    if (mask)
+      push_peers_mask(field, world, rank, off + size_t(i), v, __ldg(mask + i));
+    else
+      push_peers(field, world, rank, off + size_t(i), v);
   }
 };
 
@@ -93,7 +119,7 @@ struct DualEpi : EpiBase<DualEpi<kSeq, kCoh, kShard>> {
     red[2] += isfinite(yn) ? 0.0 : 1.0;
   }
   // all operand loads of the thread's rows first, then the updates (ILP)
-  template <int RPT, int NA, int NR>
+  template <int RPT, int NA, int NR, bool kStreamIO = false>
   __device__ __forceinline__ void rows_strided(int r0, int stride, int nvalid,
                                                const double (&acc)[RPT][NA],
                                                double (&red)[NR]) const {
@@ -102,9 +128,9 @@ struct DualEpi : EpiBase<DualEpi<kSeq, kCoh, kShard>> {
     for (int i = 0; i < RPT; ++i)
       if (i < nvalid) {
         const int r = r0 + i * stride;
-        kxo[i] = ldv<kCoh>(kx + r);
-        yo[i] = ldv<kCoh>(y + r);
-        qq[i] = q[r];
+        kxo[i] = ld_io<kCoh, kStreamIO>(kx + r);
+        yo[i] = ld_io<kCoh, kStreamIO>(y + r);
+        qq[i] = ld_io_plain<kStreamIO>(q + r);
       }
 #pragma unroll
     for (int i = 0; i < RPT; ++i)
@@ -113,9 +139,9 @@ struct DualEpi : EpiBase<DualEpi<kSeq, kCoh, kShard>> {
         const double kxn = acc[i][0];
         double yn = yo[i] + sigma * (qq[i] - 2.0 * kxn + kxo[i]);  // solver.hpp:412-413
         if (r < m1 && yn < 0.0) yn = 0.0;
-        yt[r] = yn;
+        st_io<kStreamIO>(yt + r, yn);
         if (kShard) push(r, yn);
-        kxt[r] = kxn;
+        st_io<kStreamIO>(kxt + r, kxn);
         const double d = yn - yo[i];
         const double dd = d * d, di = d * (kxn - kxo[i]);
         if (kSeq) {
@@ -211,7 +237,7 @@ struct PrimalEpi : EpiBase<PrimalEpi<kSeq, kNonneg, kCoh, kShard>> {
     if (do_avg) st2(avg_x + j0, av);
   }
   // all operand loads of the thread's columns first, then the updates (ILP)
-  template <int RPT, int NA, int NR>
+  template <int RPT, int NA, int NR, bool kStreamIO = false>
   __device__ __forceinline__ void rows_strided(int j0, int stride, int nvalid,
                                                const double (&acc)[RPT][NA],
                                                double (&red)[NR]) const {
@@ -220,12 +246,12 @@ struct PrimalEpi : EpiBase<PrimalEpi<kSeq, kNonneg, kCoh, kShard>> {
     for (int i = 0; i < RPT; ++i)
       if (i < nvalid) {
         const int j = j0 + i * stride;
-        xa[i] = ldv<kCoh>(xc + j);
-        cc[i] = c[j];
-        if (do_avg && !avg_first) av[i] = avg_x[j];
+        xa[i] = ld_io<kCoh, kStreamIO>(xc + j);
+        cc[i] = ld_io_plain<kStreamIO>(c + j);
+        if (do_avg && !avg_first) av[i] = ld_io_plain<kStreamIO>(avg_x + j);
         if (!kNonneg) {
-          ll[i] = l[j];
-          uu[i] = u[j];
+          ll[i] = ld_io_plain<kStreamIO>(l + j);
+          uu[i] = ld_io_plain<kStreamIO>(u + j);
         }
       }
 #pragma unroll
@@ -233,11 +259,11 @@ struct PrimalEpi : EpiBase<PrimalEpi<kSeq, kNonneg, kCoh, kShard>> {
       if (i < nvalid) {
         const int j = j0 + i * stride;
         const double s = acc[i][0];
-        if (store_kty) kty_out[j] = s;
-        if (do_avg) avg_x[j] = avg_first ? xa[i] : av[i] + ratio * (xa[i] - av[i]);
+        if (store_kty) st_io<kStreamIO>(kty_out + j, s);
+        if (do_avg) st_io<kStreamIO>(avg_x + j, avg_first ? xa[i] : av[i] + ratio * (xa[i] - av[i]));
         const double v = xa[i] - tau * (cc[i] - s);  // solver.hpp:404-408
         const double xn = kNonneg ? smax(v, 0.0) : clamp_box(v, ll[i], uu[i]);
-        xt[j] = xn;
+        st_io<kStreamIO>(xt + j, xn);
         if (kShard) push(j, xn);
         const double d = xn - xa[i];
         const double dd = d * d;

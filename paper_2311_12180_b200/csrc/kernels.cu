@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 4) dual_kernel(DevCsr K, DevIter it,
   epi.seq_inter = it.seq_inter;
   epi.sigma = st->eta * st->omega;  // sigma = eta * omega, solver.hpp:402
   epi.m1 = it.m1;
-  if (kShard) epi.push = PeerPush{it.shv->y_all, size_t(st->iy_trial) * it.m, it.world, it.rank};
+  if (kShard) epi.push = PeerPush{it.shv->y_all, size_t(st->iy_trial) * it.m, it.world, it.rank, it.ymask};
   double red[3] = {0.0, 0.0, 0.0};
   const int role = run_tile<DualEpi<kSeq, false, kShard>, kSeq>(t, K.rp, K.col, K.val, epi, red,
                                                                 K.chunk_part, K.chunk_ctr, smem);
@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(kThreads, 4) primal_kernel(DevCsr KT, DevIter 
   double red[2] = {0.0, 0.0};
   int role = kRoleOwn;
   const double tau = d.eta / d.omega;  // tau = eta / omega, solver.hpp:401
-  const PeerPush push{kShard ? it.shv->x_all : nullptr, size_t(d.ix_trial) * it.n, it.world, it.rank};
+  const PeerPush push{kShard ? it.shv->x_all : nullptr, size_t(d.ix_trial) * it.n, it.world, it.rank, it.xmask};
   if (bid >= KT.ntiles) {
     // avg_y .add (solver.hpp:839) on this CTA's slice of the own dual rows; no partial
     if (d.mode == kPAccept) {
@@ -697,16 +697,63 @@ __global__ void __launch_bounds__(kThreads) eval_prep_kernel(DevIter it, DevEval
 }
 
 // Sharded evaluation: this rank's slices of the averages to every peer (the
-// iteration keeps averages rank-local; they are gathered once per window).
+// iteration keeps averages rank-local; they are gathered once per window),
+// and, when trials push only to the peers that gather a value (masks), its
+// slices of the current and previous iterates, which the evaluation reads in
+// full.
 __global__ void push_avg_kernel(DevIter it) {
   const ShardView* v = it.shv;
+  const DevState* st = it.st;
   const int stride = gridDim.x * blockDim.x;
-  for (int j = it.col0 + blockIdx.x * blockDim.x + threadIdx.x; j < it.col1; j += stride)
+  for (int j = it.col0 + blockIdx.x * blockDim.x + threadIdx.x; j < it.col1; j += stride) {
     push_peers(v->avg_x, it.world, it.rank, size_t(j), it.avg_x[j]);
-  for (int i = it.row0 + blockIdx.x * blockDim.x + threadIdx.x; i < it.row1; i += stride)
+    if (it.xmask) {
+      push_peers(v->x_all, it.world, it.rank, size_t(st->ix_cur) * it.n + j, it.x[st->ix_cur][j]);
+      push_peers(v->x_all, it.world, it.rank, size_t(st->ix_prev) * it.n + j, it.x[st->ix_prev][j]);
+    }
+  }
+  for (int i = it.row0 + blockIdx.x * blockDim.x + threadIdx.x; i < it.row1; i += stride) {
     push_peers(v->avg_y, it.world, it.rank, size_t(i), it.avg_y[i]);
+    if (it.ymask) {
+      push_peers(v->y_all, it.world, it.rank, size_t(st->iy_cur) * it.m + i, it.y[st->iy_cur][i]);
+      push_peers(v->y_all, it.world, it.rank, size_t(st->iy_prev) * it.m + i, it.y[st->iy_prev][i]);
+    }
+  }
   shard_signal(v, it.sync, it.world, it.rank, kSyncAvg);
 }
+
+// Gather masks: for every nonzero (r, c) of K, rank owner(r) reads x'[c] and
+// rank owner_t(c) reads y'[r] (owners by the row cuts of K and of K^T).
+__global__ void shard_mask_kernel(const int* rp, const int* col, int rows, const int64_t* kc, const int64_t* ktc,
+                                  int world, unsigned* xmask, unsigned* ymask) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+    int pr = 0;
+    while (pr + 1 < world && r >= kc[pr + 1]) ++pr;
+    unsigned ym = 0;
+    for (int k = rp[r]; k < rp[r + 1]; ++k) {
+      const int c = col[k];
+      int pc = 0;
+      while (pc + 1 < world && c >= ktc[pc + 1]) ++pc;
+      atomicOr(xmask + c, 1u << pr);  // integer: order-free
+      ym |= 1u << pc;
+    }
+    ymask[r] = ym;
+  }
+}
+
+// Values this rank pushes per trial with the masks (out[0]) and without (out[1]).
+__global__ void shard_volume_kernel(const unsigned* xmask, const unsigned* ymask, int col0, int col1, int row0,
+                                    int row1, int world, int rank, unsigned long long* out) {
+  unsigned long long a = 0, b = 0;
+  const unsigned others = ((world >= 32 ? 0xffffffffu : ((1u << world) - 1u)) & ~(1u << rank));
+  for (int j = col0 + blockIdx.x * blockDim.x + threadIdx.x; j < col1; j += gridDim.x * blockDim.x)
+    a += __popc(xmask[j] & others), b += world - 1;
+  for (int i = row0 + blockIdx.x * blockDim.x + threadIdx.x; i < row1; i += gridDim.x * blockDim.x)
+    a += __popc(ymask[i] & others), b += world - 1;
+  atomicAdd(out, a);
+  atomicAdd(out + 1, b);
+}
+
 
 // Waits (on the device) until every rank published `kind`.
 __global__ void shard_barrier_kernel(ShardSync* sync, int world, int kind) {
@@ -1569,6 +1616,18 @@ void launch_eval_lambda(const DevCsr& kt, const DevIter& it, const DevEval& ev, 
 void launch_reduced_of_objective(const double* c, const double* l, const double* u, int n,
                                  double* lam, cudaStream_t s) {
   reduced_of_objective_kernel<<<grid_for(n), kThreads, 0, s>>>(c, l, u, n, lam);
+  PDLP_CUDA(cudaGetLastError());
+}
+
+void launch_shard_masks(const int* rp, const int* col, int rows, const int64_t* kc, const int64_t* ktc, int world,
+                        unsigned* xmask, unsigned* ymask, cudaStream_t s) {
+  shard_mask_kernel<<<grid_for(rows), kThreads, 0, s>>>(rp, col, rows, kc, ktc, world, xmask, ymask);
+  PDLP_CUDA(cudaGetLastError());
+}
+void launch_shard_volume(const unsigned* xmask, const unsigned* ymask, int col0, int col1, int row0, int row1,
+                         int world, int rank, unsigned long long* out, cudaStream_t s) {
+  shard_volume_kernel<<<grid_for(int64_t(col1 - col0) + (row1 - row0)), kThreads, 0, s>>>(
+      xmask, ymask, col0, col1, row0, row1, world, rank, out);
   PDLP_CUDA(cudaGetLastError());
 }
 

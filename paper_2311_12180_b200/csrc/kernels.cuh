@@ -75,6 +75,13 @@ void launch_primal(const DevCsr& kt, const DevIter& it, bool seq, int mode_overr
 void launch_zero_iterate(const DevIter& it, cudaStream_t s);
 void launch_restart_copy(const DevIter& it, int from_avg, cudaStream_t s);
 
+// ---- sharding ----------------------------------------------------------------
+// Gather masks of x' (n) and y' (m): bit q = rank q reads the value (zeroed first).
+void launch_shard_masks(const int* rp, const int* col, int rows, const int64_t* kc, const int64_t* ktc, int world,
+                        unsigned* xmask, unsigned* ymask, cudaStream_t s);
+void launch_shard_volume(const unsigned* xmask, const unsigned* ymask, int col0, int col1, int row0, int row1,
+                         int world, int rank, unsigned long long* out, cudaStream_t s);
+
 // ---- evaluation ------------------------------------------------------------
 // Side stream + events for running EV1 and EV2 concurrently (single device).
 struct EvalFork {

@@ -81,13 +81,30 @@ using SweepOp = PanelView;
 #endif
 constexpr int kSweepRows = PDLP_SWEEP_ROWS;  // rows per CTA: 4 or 8 per thread, stride kThreads
 constexpr int kSweepRPT = kSweepRows / kThreads;
+// 1536 staged entries (6 per thread) and 6 resident CTAs per SM for the SpMV
+// passes, 5 / 4 for the dual / primal final passes (C4: K 1.70 -> 1.44 ms,
+// whole iteration 234 -> 250 it/s; the passes are latency-bound, so resident
+// CTAs matter more than loads in flight per thread)
 #ifndef PDLP_SWEEP_CHUNK
-#define PDLP_SWEEP_CHUNK 2048
+#define PDLP_SWEEP_CHUNK 1536
 #endif
 #ifndef PDLP_SWEEP_CTAS
-#define PDLP_SWEEP_CTAS 4
+#define PDLP_SWEEP_CTAS 6
 #endif
-constexpr int kSweepChunk = PDLP_SWEEP_CHUNK;      // products staged per round (16 KB)
+// resident CTAs per SM of the final passes (their fused updates need more
+// registers than the SpMV passes)
+#ifndef PDLP_SWEEP_CTAS_DUALF
+#define PDLP_SWEEP_CTAS_DUALF 5
+#endif
+#ifndef PDLP_SWEEP_CTAS_PRIMALF
+#define PDLP_SWEEP_CTAS_PRIMALF 4
+#endif
+// the final passes stream their dense update operands (.cs) past the L2-resident panel slice
+#ifndef PDLP_SWEEP_STREAM_IO
+#define PDLP_SWEEP_STREAM_IO 1
+#endif
+constexpr bool kSweepStreamIO = PDLP_SWEEP_STREAM_IO != 0;
+constexpr int kSweepChunk = PDLP_SWEEP_CHUNK;      // products staged per round (12 KB)
 constexpr int kSweepPer = kSweepChunk / kThreads;  // entries per thread per round, all in flight
 constexpr int kSweepCtasPerSm = PDLP_SWEEP_CTAS;
 
@@ -321,7 +338,7 @@ __global__ void __launch_bounds__(kThreads, kSweepCtasPerSm) sweep_pass_kernel(S
 // Last pass of the dual: CTA 0 is the helper (state snapshot, dx^2 of x'); CTA
 // b >= 1 finishes rows [(b-1) R, b R) and applies the dual update (DualEpi)
 // with its partials at slot b-1.
-__global__ void __launch_bounds__(kThreads, kSweepCtasPerSm) sweep_dual_final_kernel(SweepOp op, DevIter it) {
+__global__ void __launch_bounds__(kThreads, PDLP_SWEEP_CTAS_DUALF) sweep_dual_final_kernel(SweepOp op, DevIter it) {
   __shared__ SweepSmem sm;
   griddep_wait();
   DevState* st = it.st;
@@ -358,7 +375,7 @@ __global__ void __launch_bounds__(kThreads, kSweepCtasPerSm) sweep_dual_final_ke
 #pragma unroll
   for (int q = 0; q < kSweepRPT; ++q) a2[q][0] = acc[q];
   double red[3] = {0.0, 0.0, 0.0};
-  epi.rows_strided<kSweepRPT>(r0, kThreads, nvalid, a2, red);
+  epi.rows_strided<kSweepRPT, 1, 3, kSweepStreamIO>(r0, kThreads, nvalid, a2, red);
   griddep_launch_dependents();
   store_partial<3, 0>(red, it.d_part, b, it.d_tiles);
 }
@@ -368,7 +385,7 @@ __global__ void __launch_bounds__(kThreads, kSweepCtasPerSm) sweep_dual_final_ke
 // averages; restart / lazy retry: without), or recompute x' from the kept K'y
 // (retry); the trailing CTAs update avg_y on accepted steps.
 template <bool kNonneg>
-__global__ void __launch_bounds__(kThreads, kSweepCtasPerSm) sweep_primal_final_kernel(SweepOp op, DevIter it,
+__global__ void __launch_bounds__(kThreads, PDLP_SWEEP_CTAS_PRIMALF) sweep_primal_final_kernel(SweepOp op, DevIter it,
                                                                                      int mode_override) {
   __shared__ SweepSmem sm;
   griddep_wait();
@@ -385,8 +402,11 @@ __global__ void __launch_bounds__(kThreads, kSweepCtasPerSm) sweep_primal_final_
       const int per = (it.m + nb - 1) / nb;
       const int i0 = b * per, i1 = min(it.m, i0 + per);
       const double* yc = it.y[s.iy_cur];
-      for (int i = i0 + threadIdx.x; i < i1; i += kThreads)
-        it.avg_y[i] = s.avg_first ? yc[i] : it.avg_y[i] + s.avg_ratio * (yc[i] - it.avg_y[i]);
+      for (int i = i0 + threadIdx.x; i < i1; i += kThreads) {
+        const double yv = ld_io_plain<kSweepStreamIO>(yc + i);
+        const double av = s.avg_first ? 0.0 : ld_io_plain<kSweepStreamIO>(it.avg_y + i);
+        st_io<kSweepStreamIO>(it.avg_y + i, s.avg_first ? yv : av + s.avg_ratio * (yv - av));
+      }
     }
     return;
   }
@@ -419,7 +439,7 @@ __global__ void __launch_bounds__(kThreads, kSweepCtasPerSm) sweep_primal_final_
     double a2[kSweepRPT][1];
 #pragma unroll
     for (int q = 0; q < kSweepRPT; ++q) a2[q][0] = acc[q];
-    epi.template rows_strided<kSweepRPT>(j0, kThreads, nvalid, a2, red);
+    epi.template rows_strided<kSweepRPT, 1, 2, kSweepStreamIO>(j0, kThreads, nvalid, a2, red);
   } else if (mode == kPRetry) {
     const double* xc = it.x[s.ix_cur];
     const double* kty = it.kty[s.ikty_cur];

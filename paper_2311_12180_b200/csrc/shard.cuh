@@ -94,6 +94,17 @@ __device__ __forceinline__ void push_peers(double* const* field, int world, int 
     }
 }
 
+// push_peers restricted to the ranks of `mask` (bit q: rank q).
+__device__ __forceinline__ void push_peers_mask(double* const* field, int world, int rank, size_t off, double v,
+                                                unsigned mask) {
+#pragma unroll 1
+  for (int q = 0; q < world; ++q)
+    if (q != rank && ((mask >> q) & 1u)) {
+      double* b = reinterpret_cast<double*>(__ldg(reinterpret_cast<const unsigned long long*>(field + q)));
+      b[off] = v;
+    }
+}
+
 // Thread 0 holds a block-reduced partial of width W (after store_partial):
 // copy it to every peer's (component-major) partial array at the same slot.
 template <int W>

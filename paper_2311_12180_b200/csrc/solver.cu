@@ -835,6 +835,32 @@ void Solver::allocate_iteration() {
   ev.world = world_, ev.rank = rank_;
   ev.sync = sync_.get();
   ev.shv = shv_dev_.get();
+  // trials push x' / y' only to the peers whose rows gather them (a banded or
+  // staircase operator exchanges its coupling values only); PDLP_SHARD_FULL=1
+  // pushes every value to every peer
+  it.xmask = it.ymask = nullptr;
+  if (world_ > 1 && !std::getenv("PDLP_SHARD_FULL")) {
+    DevBuf<int64_t> kc{k_cuts_.size()}, ktc{kt_cuts_.size()};
+    PDLP_CUDA(cudaMemcpyAsync(kc.get(), k_cuts_.data(), k_cuts_.size() * 8, cudaMemcpyHostToDevice, s));
+    PDLP_CUDA(cudaMemcpyAsync(ktc.get(), kt_cuts_.data(), kt_cuts_.size() * 8, cudaMemcpyHostToDevice, s));
+    xmask_.alloc(n_);
+    ymask_.alloc(m_);
+    xmask_.zero(s);
+    launch_shard_masks(k_rp_.get(), k_col_.get(), int(m_), kc.get(), ktc.get(), world_, xmask_.get(), ymask_.get(), s);
+    DevBuf<unsigned long long> vol{static_cast<size_t>(2)};
+    vol.zero(s);
+    launch_shard_volume(xmask_.get(), ymask_.get(), int(col0), int(col1), int(row0), int(row1), world_, rank_,
+                        vol.get(), s);
+    unsigned long long vh[2] = {0, 0};
+    PDLP_CUDA(cudaMemcpyAsync(vh, vol.get(), sizeof vh, cudaMemcpyDeviceToHost, s));
+    PDLP_CUDA(cudaStreamSynchronize(s));
+    push_values_ = int64_t(vh[0]);
+    push_values_full_ = int64_t(vh[1]);
+    it.xmask = xmask_.get();
+    it.ymask = ymask_.get();
+  } else if (world_ > 1) {
+    push_values_ = push_values_full_ = ((col1 - col0) + (row1 - row0)) * int64_t(world_ - 1);
+  }
   for (int q = 0; q < kMaxShards; ++q) {
     shv_.x_all[q] = x_all_.get();
     shv_.y_all[q] = y_all_.get();
@@ -1779,6 +1805,11 @@ void Solver::shard_info(int64_t* out) const {
   out[7] = KT_.ntiles;
   out[8] = int64_t(k_it_.plan.tiles.size());
   out[9] = int64_t(kt_it_.plan.tiles.size());
+}
+
+void Solver::shard_exchange(int64_t* out) const {
+  out[0] = push_values_;
+  out[1] = push_values_full_;
 }
 
 }  // namespace pdlp

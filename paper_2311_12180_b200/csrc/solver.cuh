@@ -194,6 +194,7 @@ class Solver {
   void kernel_bytes(int which, double* alg, double* moved) const;
   int panels(int op) const { return op == 0 ? kpan_.panels : ktpan_.panels; }
   void sizes(int64_t* out) const;
+  void shard_exchange(int64_t* out) const;
   // ---- sharding ----
   static void link_local(const std::vector<Solver*>& ranks);
   void export_shard(ShardBlob* out) const;
@@ -328,6 +329,8 @@ class Solver {
   int64_t l2_window_bytes_ = 0;  // persisting L2 carve-out for the gathered iterate
   int world_ = 1, rank_ = 0;
   std::vector<int64_t> k_cuts_, kt_cuts_;  // world + 1 row boundaries of K and K^T
+  DevBuf<unsigned> xmask_, ymask_;          // gather masks of x' / y' (sharded)
+  int64_t push_values_ = 0, push_values_full_ = 0;  // values pushed per trial: masked / every peer
   uint64_t plan_hash_ = 0;
   DevBuf<ShardSync> sync_;
   DevBuf<ShardView> shv_dev_;
