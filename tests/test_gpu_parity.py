@@ -220,6 +220,57 @@ def test_fast_mode_first_100_iterates(which):
     assert worst <= 1e-10, f"worst relative iterate error {worst}"
 
 
+def reorder_floor(lp, iters: int) -> tuple[float, float]:
+    """The oracle against itself with pairwise step-size sums (sum order 1):
+    how far a reordering alone moves the reference's first iterates."""
+    a = O.Session(lp, SolverParams(), "oracle")
+    O.set_sum_order(1)
+    try:
+        b = O.Session(lp, SolverParams(), "oracle")
+        w2 = wi = 0.0
+        for _ in range(iters):
+            O.set_sum_order(0)
+            a.run(1)
+            O.set_sum_order(1)
+            b.run(1)
+            ia, ib = a.iterate(), b.iterate()
+            za, zb = np.concatenate([ia["x"], ia["y"]]), np.concatenate([ib["x"], ib["y"]])
+            w2 = max(w2, float(np.linalg.norm(zb - za) / max(np.linalg.norm(za), 1e-300)))
+            wi = max(wi, rel_err(zb, za))
+        b.close()
+    finally:
+        O.set_sum_order(0)
+    a.close()
+    return w2, wi
+
+
+@pytest.mark.parametrize("which", ["staircase", "multicommodity"])
+def test_fast_mode_drift_small_tile_band(which):
+    """Structured operators in the 64k-256k nnz band, where the iteration
+    tiles are 1024-nnz STREAM tiles (solver.cu build_plan): the first 100
+    iterates within 1e-10, or within 4x the reference's own reordering drift
+    on the same instance where that floor is higher."""
+    lp = {"staircase": lambda: generators.staircase_lp(3, 5000, 1250, 1250, seed=12),
+          "multicommodity": lambda: generators.multicommodity_lp(600, 4000, 6, seed=13)}[which]()
+    assert (1 << 16) <= lp.nnz < (1 << 18), lp.nnz
+    ref = O.Session(lp, SolverParams(), "oracle")
+    w2 = wi = 0.0
+    with Solver(lp, SolverParams()) as s:
+        s.iterate_begin()
+        for _ in range(100):
+            s.iterate_run(1)
+            ref.run(1)
+            a, b = s.iterate(), ref.iterate()
+            assert (a["total"], a["inner"]) == (b["total"], b["inner"])
+            za, zb = np.concatenate([a["x"], a["y"]]), np.concatenate([b["x"], b["y"]])
+            w2 = max(w2, float(np.linalg.norm(za - zb) / max(np.linalg.norm(zb), 1e-300)))
+            wi = max(wi, rel_err(za, zb))
+    ref.close()
+    f2, fi = reorder_floor(lp, 100)
+    print(f"{which} nnz {lp.nnz}: fast {w2:.3e} / {wi:.3e}, reorder floor {f2:.3e} / {fi:.3e}")
+    assert w2 <= max(1e-10, 4.0 * f2) and wi <= max(1e-10, 4.0 * fi), (w2, wi, f2, fi)
+
+
 @pytest.mark.parametrize("which", ["C1", "transport", "rand09", "blend"])
 def test_fast_mode_solve_status_and_objective(which):
     lp = {"C1": lambda: generators.config("C1"), "transport": lambda: generators.transport_lp(60, 80, seed=11),
