@@ -283,6 +283,16 @@ int pdlp_get_iterate(pdlp_handle* h, double* x, double* y, double* kx, double* k
  * algorithmic bytes one launch moves. */
 int pdlp_time_kernel(pdlp_handle* h, int32_t which, int32_t reps, double* avg_ms,
                      double* bytes_per_launch);
+/* One plain PDHG step with explicit extrapolation, pdhg_raw_step
+ * (solver.hpp:335-358), on the handle's UNSCALED saddle problem
+ * (to_saddle(lp), lp_model.hpp:88-98): x' = clamp(x - tau (c - K'y)),
+ * y' = proj(y + sigma (q - K(2x' - x))). x, x_out: n; y, y_out: m (host).
+ * Parity mode: bitwise equal to the reference; fast mode: the tiled engine's
+ * row sums. Test-facing in the reference (test_solver.cpp:33-61); not used by
+ * pdlp_solve. */
+int pdlp_pdhg_raw_step(pdlp_handle* h, const double* x, const double* y, double tau, double sigma,
+                       double* x_out, double* y_out);
+
 /* Bytes of one launch of kernel `which` (0 dual, 1 primal, 2 SpMV K x, 3 SpMV
  * K^T y): out[0] = SURVEY.md §8(d)'s algorithmic bytes (what pdlp_time_kernel
  * reports), out[1] = the bytes the launched variant moves at one DRAM access

@@ -391,6 +391,19 @@ class Solver {
     return out;
   }
 
+  /// pdhg_raw_step (solver.hpp:335-358) on the unscaled saddle problem: one
+  /// plain PDHG step from z with explicit extrapolation 2x' - x.
+  PrimalDualPoint pdhg_raw_step(const PrimalDualPoint& z, double tau, double sigma) {
+    if (static_cast<index_t>(z.primal.size()) != n_ || static_cast<index_t>(z.dual.size()) != m_)
+      throw std::invalid_argument("pdhg_raw_step: dimension mismatch");
+    PrimalDualPoint next;
+    next.primal.resize(z.primal.size());
+    next.dual.resize(z.dual.size());
+    detail::check(pdlp_pdhg_raw_step(h_, z.primal.data(), z.dual.data(), tau, sigma, next.primal.data(),
+                                     next.dual.data()));
+    return next;
+  }
+
   /// Row sharding, one process per GPU: export this rank's blob, all-gather
   /// the blobs (MPI, torch.distributed, files), import them in rank order.
   std::vector<unsigned char> shard_export() const {

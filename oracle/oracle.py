@@ -65,6 +65,7 @@ def load(kind: str = "oracle") -> C.CDLL:
                                     dp, i64p]),
         "last_error": (C.c_char_p, []),
         "check_termination": (C.c_int, [LPP, dp, dp, C.c_double, dp]),
+        "pdhg_raw_step": (C.c_int, [LPP, dp, dp, C.c_double, C.c_double, dp, dp]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(lib, p + name)
@@ -245,6 +246,20 @@ def check_termination(lp: GeneralFormLp, x, y, eps: float, kind: str = "oracle")
     _err(lib, kind, _f(lib, kind, "check_termination")(C.byref(lpa), abi.dptr(x), abi.dptr(y), eps, abi.dptr(out)))
     return {"terminated": bool(out[0]), "primal_residual_norm": out[1], "dual_residual_norm": out[2],
             "primal_objective_raw": out[3], "dual_objective_raw": out[4]}
+
+
+def pdhg_raw_step(lp: GeneralFormLp, x, y, tau: float, sigma: float, kind: str = "oracle"):
+    """pdhg_raw_step (solver.hpp:335-358) on to_saddle(lp): returns (x', y')."""
+    lib = load(kind)
+    lpa = lp.to_abi()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    xo, yo = np.empty(lp.num_variables), np.empty(lp.num_constraints)
+    dp = C.POINTER(C.c_double)
+    _err(lib, kind, _f(lib, kind, "pdhg_raw_step")(C.byref(lpa), x.ctypes.data_as(dp), y.ctypes.data_as(dp),
+                                                 float(tau), float(sigma), xo.ctypes.data_as(dp),
+                                                 yo.ctypes.data_as(dp)))
+    return xo, yo
 
 
 def read_mps(path: str | os.PathLike) -> GeneralFormLp:

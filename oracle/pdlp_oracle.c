@@ -1327,6 +1327,41 @@ int oracle_check_termination(const pdlp_lp* lpin, const double* x, const double*
   return PDLP_OK;
 }
 
+/* pdhg_raw_step (solver.hpp:335-358) on to_saddle(lp) (lp_model.hpp:88-98):
+ * x' = clamp(x - tau (c - K'y)), then y' = proj(y + sigma (q - K (2x' - x))). */
+int oracle_pdhg_raw_step(const pdlp_lp* lpin, const double* x, const double* y, double tau, double sigma,
+                         double* xo, double* yo) {
+  lp_t lp;
+  int rc = lp_from_abi(lpin, &lp);
+  if (rc) {
+    lp_free(&lp);
+    return rc;
+  }
+  csr_t K = csr_vstack(&lp.G, &lp.A);
+  const int64_t n = lp.n, m = lp.m1 + lp.m2;
+  double* kty = dvec(n);
+  double* ext = dvec(n);
+  double* kext = dvec(m);
+  spmv_t(&K, y, kty);
+  for (int64_t i = 0; i < n; ++i) {
+    const double v = x[i] - tau * (lp.c[i] - kty[i]);
+    xo[i] = smin(smax(v, lp.l[i]), lp.u[i]); /* clamp_to_box, vector_ops.hpp:52-58 */
+  }
+  for (int64_t i = 0; i < n; ++i) ext[i] = 2.0 * xo[i] - x[i];
+  spmv(&K, ext, kext);
+  for (int64_t i = 0; i < m; ++i) {
+    const double q = i < lp.m1 ? lp.h[i] : lp.b[i - lp.m1];
+    yo[i] = y[i] + sigma * (q - kext[i]);
+  }
+  project_dual(yo, lp.m1);
+  free(kty);
+  free(ext);
+  free(kext);
+  csr_free(&K);
+  lp_free(&lp);
+  return PDLP_OK;
+}
+
 int oracle_from_triplets(int64_t rows, int64_t cols, int64_t nt, const int64_t* tr, const int64_t* tc,
                          const double* tv, int64_t* off, int64_t* col, double* val, int64_t* nnz_out) {
   csr_t m;

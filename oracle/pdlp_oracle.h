@@ -63,6 +63,10 @@ int oracle_from_triplets(int64_t rows, int64_t cols, int64_t nt, const int64_t* 
 int oracle_check_termination(const pdlp_lp* lp, const double* x, const double* y, double eps,
                              double* out);
 
+/* pdhg_raw_step (solver.hpp:335-358) on the unscaled saddle problem. */
+int oracle_pdhg_raw_step(const pdlp_lp* lp, const double* x, const double* y, double tau, double sigma,
+                         double* x_out, double* y_out);
+
 const char* oracle_last_error(void);
 
 /* Summation-order probe: 0 (default) the reference's sequential step-size

@@ -560,6 +560,25 @@ int ref_check_termination(const pdlp_lp* lp, const double* x, const double* y, d
   }
 }
 
+// pdhg_raw_step (solver.hpp:335-358) on to_saddle(lp), the unscaled saddle
+// problem, from (x, y).
+int ref_pdhg_raw_step(const pdlp_lp* lp, const double* x, const double* y, double tau, double sigma,
+                      double* x_out, double* y_out) {
+  try {
+    const GeneralFormLp g = to_lp(*lp);
+    const SaddleProblem sp = to_saddle(g);
+    PrimalDualPoint z;
+    z.primal.assign(x, x + g.num_variables());
+    z.dual.assign(y, y + g.num_constraints());
+    const PrimalDualPoint nx = pdhg_raw_step(z, tau, sigma, sp);
+    std::copy(nx.primal.begin(), nx.primal.end(), x_out);
+    std::copy(nx.dual.begin(), nx.dual.end(), y_out);
+    return PDLP_OK;
+  } catch (const std::exception& e) {
+    return fail(PDLP_EINVAL, e.what());
+  }
+}
+
 // MPS loading through the reference parser (fixture generation only).
 // Two-phase: ref_mps_load parses and keeps the instance; ref_mps_sizes reports
 // {n, m1, m2, nnzG, nnzA}; ref_mps_fill copies into caller buffers.

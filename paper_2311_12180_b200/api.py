@@ -79,6 +79,7 @@ def load_library(build_if_missing: bool = True) -> C.CDLL:
         "pdlp_shard_import": (C.c_int, [H, C.c_void_p, C.c_int32]),
         "pdlp_shard_info": (C.c_int, [H, i64p]),
         "pdlp_shard_exchange": (C.c_int, [H, i64p]),
+        "pdlp_pdhg_raw_step": (C.c_int, [H, dp, dp, C.c_double, C.c_double, dp, dp]),
         "pdlp_plan_shards": (C.c_int, [C.POINTER(abi.PdlpLp), C.c_int32, i64p, i64p]),
     }
     for name, (res, args) in sig.items():
@@ -200,6 +201,19 @@ class Solver:
             "total": int(cnt[0]), "inner": int(cnt[1]), "outer": int(cnt[2]), "trials": int(cnt[3]),
             "eta": sc[0], "eta_hat": sc[1], "omega": sc[2], "weight_sum": sc[3],
         }
+
+    def pdhg_raw_step(self, x, y, tau: float, sigma: float) -> tuple[np.ndarray, np.ndarray]:
+        """pdhg_raw_step (solver.hpp:335-358) on the unscaled saddle problem:
+        one plain PDHG step from (x, y), returning (x', y')."""
+        n, m = self.n, self.m
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        if x.size != n or y.size != m:
+            raise ValueError("pdhg_raw_step: dimension mismatch")
+        xo, yo = np.empty(n), np.empty(m)
+        _check(self._lib.pdlp_pdhg_raw_step(self._h, abi.dptr(x), abi.dptr(y), float(tau), float(sigma),
+                                            abi.dptr(xo), abi.dptr(yo)))
+        return xo, yo
 
     # ---- row sharding ----
     def shard_info(self) -> dict:

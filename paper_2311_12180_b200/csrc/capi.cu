@@ -245,6 +245,18 @@ int pdlp_shard_info(pdlp_handle* h, int64_t* out) {
   return guarded([&] { h->solver->shard_info(out); });
 }
 
+int pdlp_pdhg_raw_step(pdlp_handle* h, const double* x, const double* y, double tau, double sigma,
+                       double* x_out, double* y_out) {
+  if (!h) return null_handle();
+  return guarded([&] {
+    int64_t sz[4];
+    h->solver->sizes(sz);
+    if ((sz[0] && (!x || !x_out)) || (sz[1] && (!y || !y_out)))
+      throw std::invalid_argument("pdhg_raw_step: null vector");
+    h->solver->pdhg_raw_step(x, y, tau, sigma, x_out, y_out);
+  });
+}
+
 int pdlp_shard_exchange(pdlp_handle* h, int64_t* out) {
   if (!h) return null_handle();
   if (!out) {

@@ -1631,4 +1631,34 @@ void launch_shard_volume(const unsigned* xmask, const unsigned* ymask, int col0,
   PDLP_CUDA(cudaGetLastError());
 }
 
+// pdhg_raw_step (solver.hpp:335-358), its elementwise halves on the unscaled
+// saddle problem: x' = clamp(x - tau (c - K'y)) and the extrapolation 2x' - x;
+// then y' = proj(y + sigma (q - K ext)) on the first m1 rows.
+__global__ void raw_primal_kernel(const double* x, const double* kty, const double* c, const double* l,
+                                  const double* u, double tau, int64_t n, double* xo, double* ext) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const double xn = clamp_box(x[i] - tau * (c[i] - kty[i]), l[i], u[i]);
+    xo[i] = xn;
+    ext[i] = 2.0 * xn - x[i];
+  }
+}
+__global__ void raw_dual_kernel(const double* y, const double* kext, const double* q, double sigma, int64_t m,
+                                int64_t m1, double* yo) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x) {
+    double yn = y[i] + sigma * (q[i] - kext[i]);
+    if (i < m1 && yn < 0.0) yn = 0.0;  // project_dual_in_place, lp_model.hpp:124-129
+    yo[i] = yn;
+  }
+}
+void launch_raw_primal(const double* x, const double* kty, const double* c, const double* l, const double* u,
+                       double tau, int64_t n, double* xo, double* ext, cudaStream_t s) {
+  raw_primal_kernel<<<grid_for(n), kThreads, 0, s>>>(x, kty, c, l, u, tau, n, xo, ext);
+  PDLP_CUDA(cudaGetLastError());
+}
+void launch_raw_dual(const double* y, const double* kext, const double* q, double sigma, int64_t m, int64_t m1,
+                     double* yo, cudaStream_t s) {
+  raw_dual_kernel<<<grid_for(m), kThreads, 0, s>>>(y, kext, q, sigma, m, m1, yo);
+  PDLP_CUDA(cudaGetLastError());
+}
+
 }  // namespace pdlp

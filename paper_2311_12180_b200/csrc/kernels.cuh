@@ -75,6 +75,12 @@ void launch_primal(const DevCsr& kt, const DevIter& it, bool seq, int mode_overr
 void launch_zero_iterate(const DevIter& it, cudaStream_t s);
 void launch_restart_copy(const DevIter& it, int from_avg, cudaStream_t s);
 
+// ---- pdhg_raw_step (solver.hpp:335-358) ---------------------------------------
+void launch_raw_primal(const double* x, const double* kty, const double* c, const double* l, const double* u,
+                       double tau, int64_t n, double* xo, double* ext, cudaStream_t s);
+void launch_raw_dual(const double* y, const double* kext, const double* q, double sigma, int64_t m, int64_t m1,
+                     double* yo, cudaStream_t s);
+
 // ---- sharding ----------------------------------------------------------------
 // Gather masks of x' (n) and y' (m): bit q = rank q reads the value (zeroed first).
 void launch_shard_masks(const int* rp, const int* col, int rows, const int64_t* kc, const int64_t* ktc, int world,

@@ -1807,6 +1807,33 @@ void Solver::shard_info(int64_t* out) const {
   out[9] = int64_t(kt_it_.plan.tiles.size());
 }
 
+// pdhg_raw_step (solver.hpp:335-358) from (x, y) on the unscaled saddle
+// problem to_saddle(lp) (original values of K, c, l, u, q): K'y, the primal
+// half with the extrapolation, K ext, the dual half. Parity mode sums every
+// row sequentially (bitwise with the reference); fast mode uses the tiled
+// engine's reduction order.
+void Solver::pdhg_raw_step(const double* x, const double* y, double tau, double sigma, double* xo, double* yo) {
+  if (world_ > 1) throw std::logic_error("pdhg_raw_step: single-device handles only");
+  if (!(tau > 0.0) || !(sigma > 0.0) || !std::isfinite(tau) || !std::isfinite(sigma))
+    invalid("pdhg_raw_step: tau and sigma must be positive and finite");
+  PDLP_CUDA(cudaSetDevice(params_.device));
+  cudaStream_t s = stream_;
+  DevBuf<double> dx(n_), dy(m_), kty(n_), ext(n_), kext(m_), dxo(n_), dyo(m_);
+  if (n_) PDLP_CUDA(cudaMemcpyAsync(dx.get(), x, n_ * sizeof(double), cudaMemcpyHostToDevice, s));
+  if (m_) PDLP_CUDA(cudaMemcpyAsync(dy.get(), y, m_ * sizeof(double), cudaMemcpyHostToDevice, s));
+  if (n_) launch_fill(kty.get(), n_, 0.0, s);
+  launch_spmv(KT_, true, dy.get(), kty.get(), parity(), s);  // spmv_transpose, solver.hpp:341
+  launch_raw_primal(dx.get(), kty.get(), c_orig_.get(), l_orig_.get(), u_orig_.get(), tau, n_, dxo.get(), ext.get(),
+                    s);
+  if (m_) launch_fill(kext.get(), m_, 0.0, s);
+  launch_spmv(K_, true, ext.get(), kext.get(), parity(), s);  // spmv, solver.hpp:352
+  launch_raw_dual(dy.get(), kext.get(), q_orig_.get(), sigma, m_, m1_, dyo.get(), s);
+  if (n_) PDLP_CUDA(cudaMemcpyAsync(xo, dxo.get(), n_ * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (m_) PDLP_CUDA(cudaMemcpyAsync(yo, dyo.get(), m_ * sizeof(double), cudaMemcpyDeviceToHost, s));
+  PDLP_CUDA(cudaStreamSynchronize(s));
+  launches_ += 4;
+}
+
 void Solver::shard_exchange(int64_t* out) const {
   out[0] = push_values_;
   out[1] = push_values_full_;

@@ -195,6 +195,7 @@ class Solver {
   int panels(int op) const { return op == 0 ? kpan_.panels : ktpan_.panels; }
   void sizes(int64_t* out) const;
   void shard_exchange(int64_t* out) const;
+  void pdhg_raw_step(const double* x, const double* y, double tau, double sigma, double* xo, double* yo);
   // ---- sharding ----
   static void link_local(const std::vector<Solver*>& ranks);
   void export_shard(ShardBlob* out) const;

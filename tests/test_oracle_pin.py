@@ -254,3 +254,24 @@ def test_c2_reorder_drift_matches_committed_floor():
     got = mgc.reorder_drift("C2", generators.config("C2"))
     assert got["rel2"] == meta["reorder_drift"]["rel2"] and got["relinf"] == meta["reorder_drift"]["relinf"]
     assert got["rel2"] > 0.0
+
+
+def test_oracle_pdhg_raw_step_known_answers_and_reference():
+    """pdhg_raw_step (solver.hpp:335-358): the reference's hand traces
+    (test_solver.cpp:33-61) and bitwise equality with the reference compiled
+    in place on a seeded LP."""
+    from tests.test_gpu_raw_step import one_var_lp, origin_lp
+
+    x, y = O.pdhg_raw_step(origin_lp(), np.zeros(2), np.zeros(1), 0.7, 0.3)
+    assert x.tolist() == [0.0, 0.0] and y.tolist() == [0.0]
+    x, y = O.pdhg_raw_step(one_var_lp(), np.zeros(1), np.zeros(1), 0.5, 0.5)
+    assert x.tolist() == [0.0] and y.tolist() == [0.5]
+    x, y = O.pdhg_raw_step(one_var_lp(), np.ones(1), np.ones(1), 0.4, 0.9)
+    assert x.tolist() == [1.0] and y.tolist() == [1.0]
+    if not O.available("ref"):
+        pytest.skip("oracle/_ref not built")
+    lp = generators.random_lp(60, 40, 150, 4, seed=9)
+    rng = np.random.default_rng(9)
+    xs, ys = rng.uniform(-1, 3, lp.num_variables), rng.uniform(-2, 2, lp.num_constraints)
+    a, b = O.pdhg_raw_step(lp, xs, ys, 0.3, 0.7), O.pdhg_raw_step(lp, xs, ys, 0.3, 0.7, "ref")
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
