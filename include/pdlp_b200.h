@@ -377,10 +377,12 @@ int pdlp_shard_export(pdlp_handle* h, void* blob, int64_t capacity);
 int pdlp_shard_import(pdlp_handle* h, const void* blobs, int32_t world);
 /* {world, rank, row0, row1, col0, col1, own K tiles, own K^T tiles, K tiles, K^T tiles} */
 int pdlp_shard_info(pdlp_handle* h, int64_t* out);
-/* Per-trial exchange of this rank: out[0] = x' and y' values it pushes to
- * peers (only to the ranks whose rows gather each value, SURVEY §8e's
- * coupling-only exchange), out[1] = the values an all-to-all push would send
- * ((own columns + own rows) * (world - 1)). 8 bytes each. (new) */
+/* Per-trial exchange and storage of this rank: out[0] = x' and y' values it
+ * pushes to peers (only to the ranks whose rows gather each value, SURVEY
+ * §8e's coupling-only exchange), out[1] = the values an all-to-all push would
+ * send ((own columns + own rows) * (world - 1)), 8 bytes each; out[2], out[3]
+ * = nonzeros of K and of K^T stored on this rank (a rank keeps only its own
+ * rows after setup). `out` holds 4 values. (new) */
 int pdlp_shard_exchange(pdlp_handle* h, int64_t* out);
 /* Host-only: the row cuts (world + 1 each) of K = (G; A) and of K^T that a
  * world-way sharded solve of `lp` uses. No device work. */

@@ -224,11 +224,12 @@ class Solver:
         return {k: int(v) for k, v in zip(keys, out)}
 
     def shard_exchange(self) -> dict:
-        """Values this rank pushes to peers per trial: with the gather masks
-        and with an all-to-all push (pdlp_shard_exchange)."""
-        out = np.zeros(2, np.int64)
+        """Values this rank pushes to peers per trial (with the gather masks,
+        and with an all-to-all push) and the nonzeros of K and K^T it stores
+        (pdlp_shard_exchange)."""
+        out = np.zeros(4, np.int64)
         _check(self._lib.pdlp_shard_exchange(self._h, abi.i64ptr(out)))
-        return {"pushed": int(out[0]), "all_to_all": int(out[1])}
+        return {"pushed": int(out[0]), "all_to_all": int(out[1]), "k_nnz": int(out[2]), "kt_nnz": int(out[3])}
 
     def shard_export(self) -> bytes:
         size = int(self._lib.pdlp_shard_blob_size())

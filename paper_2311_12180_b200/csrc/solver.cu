@@ -861,6 +861,9 @@ void Solver::allocate_iteration() {
   } else if (world_ > 1) {
     push_values_ = push_values_full_ = ((col1 - col0) + (row1 - row0)) * int64_t(world_ - 1);
   }
+  // a rank keeps only its own rows of K and K^T from here on (the setup above
+  // needed all of them: scaling, plans, gather masks)
+  if (world_ > 1 && !std::getenv("PDLP_SHARD_KEEP_ALL")) compact_own_rows();
   for (int q = 0; q < kMaxShards; ++q) {
     shv_.x_all[q] = x_all_.get();
     shv_.y_all[q] = y_all_.get();
@@ -1479,7 +1482,8 @@ void Solver::get_iterate(double* x, double* y, double* kx, double* kty, int64_t*
   if (kty && n_) {
     // lazily kept K'y': recompute it for the current y (same tiles and order
     // as the primal kernel, so bitwise what it would have stored)
-    if (it_.kty_lazy) launch_spmv(KT_full_, false, it_.y[st.iy_cur], it_.kty[st.ikty_cur], parity(), s);
+    if (it_.kty_lazy)
+      launch_spmv(compacted_ ? KT_ : KT_full_, false, it_.y[st.iy_cur], it_.kty[st.ikty_cur], parity(), s);
     PDLP_CUDA(cudaMemcpyAsync(kty, kty_[st.ikty_cur].get(), n_ * 8, cudaMemcpyDeviceToHost, s));
   }
   PDLP_CUDA(cudaStreamSynchronize(s));
@@ -1528,6 +1532,7 @@ void Solver::get_scaling(double* row_scale, double* col_scale) const {
 }
 
 void Solver::spmv(int op, const double* in, double* out) {
+  if (compacted_) throw std::logic_error("spmv: a sharded rank keeps only its own rows of the operators");
   const bool transpose = op == PDLP_OP_KT_SCALED || op == PDLP_OP_KT_ORIGINAL;
   const bool orig = op == PDLP_OP_K_ORIGINAL || op == PDLP_OP_KT_ORIGINAL;
   if (op < 0 || op > 3) invalid("spmv: unknown operator");
@@ -1794,6 +1799,60 @@ void Solver::import_shards(const ShardBlob* blobs, int world) {
   linked_ = true;  // in-kernel flag barriers order the ranks
 }
 
+// Per-rank operator storage: copies this rank's rows of K (rows [k_cuts_[r],
+// k_cuts_[r+1])) and of K^T (rows [kt_cuts_[r], kt_cuts_[r+1])) into compact
+// arrays and frees the full ones. The device views keep global row and entry
+// indices (the tiles store them): their pointers are the compact arrays offset
+// by the first own row / entry, so every kernel runs unchanged on own tiles.
+void Solver::compact_own_rows() {
+  cudaStream_t s = stream_;
+  auto compact = [&](DevBuf<int>& rp, DevBuf<int>& col, DevBuf<double>& val, DevBuf<double>& val_orig,
+                     int64_t r0, int64_t r1, std::initializer_list<DevCsr*> views) {
+    // the kernels' vector loads need the global alignment: starts rounded
+    // down to a multiple of 8 rows / entries
+    int k01[3] = {0, 0, 0};
+    PDLP_CUDA(cudaMemcpyAsync(&k01[2], rp.get() + r0, sizeof(int), cudaMemcpyDeviceToHost, s));
+    r0 &= ~int64_t(7);
+    PDLP_CUDA(cudaMemcpyAsync(&k01[0], rp.get() + r0, sizeof(int), cudaMemcpyDeviceToHost, s));
+    PDLP_CUDA(cudaMemcpyAsync(&k01[1], rp.get() + r1, sizeof(int), cudaMemcpyDeviceToHost, s));
+    PDLP_CUDA(cudaStreamSynchronize(s));
+    const int64_t k0 = int64_t(k01[0]) & ~int64_t(7), k1 = k01[1], rows = r1 - r0, nz = k1 - k0;
+    const int64_t own = k1 - k01[2];  // entries of the own rows (the copy starts a few earlier)
+    DevBuf<int> rp_o(size_t(rows + 1) + kVecPad), col_o(size_t(nz) + kVecPad);
+    DevBuf<double> val_o(size_t(nz) + kVecPad), vor_o(size_t(nz) + kVecPad);
+    rp_o.zero(s);
+    col_o.zero(s);
+    val_o.zero(s);
+    vor_o.zero(s);
+    PDLP_CUDA(cudaMemcpyAsync(rp_o.get(), rp.get() + r0, size_t(rows + 1) * sizeof(int), cudaMemcpyDeviceToDevice, s));
+    if (nz) {
+      PDLP_CUDA(cudaMemcpyAsync(col_o.get(), col.get() + k0, size_t(nz) * sizeof(int), cudaMemcpyDeviceToDevice, s));
+      PDLP_CUDA(cudaMemcpyAsync(val_o.get(), val.get() + k0, size_t(nz) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      PDLP_CUDA(cudaMemcpyAsync(vor_o.get(), val_orig.get() + k0, size_t(nz) * sizeof(double),
+                                cudaMemcpyDeviceToDevice, s));
+    }
+    PDLP_CUDA(cudaStreamSynchronize(s));
+    rp = std::move(rp_o);
+    col = std::move(col_o);
+    val = std::move(val_o);
+    val_orig = std::move(vor_o);
+    for (DevCsr* v : views) {
+      v->rp = rp.get() - r0;
+      v->col = col.get() - k0;
+      v->val = val.get() - k0;
+      v->val_orig = val_orig.get() - k0;
+    }
+    return own;
+  };
+  const int64_t own_k = compact(k_rp_, k_col_, k_val_, k_val_orig_, k_cuts_[rank_], k_cuts_[rank_ + 1],
+                                {&K_, &K_full_, &k_it_.csr, &k_ev_.csr});
+  const int64_t own_kt = compact(kt_rp_, kt_col_, kt_val_, kt_val_orig_, kt_cuts_[rank_], kt_cuts_[rank_ + 1],
+                                 {&KT_, &KT_full_, &kt_it_.csr, &kt_ev_.csr});
+  own_nnz_[0] = own_k;
+  own_nnz_[1] = own_kt;
+  compacted_ = true;
+}
+
 void Solver::shard_info(int64_t* out) const {
   out[0] = world_;
   out[1] = rank_;
@@ -1837,6 +1896,8 @@ void Solver::pdhg_raw_step(const double* x, const double* y, double tau, double 
 void Solver::shard_exchange(int64_t* out) const {
   out[0] = push_values_;
   out[1] = push_values_full_;
+  out[2] = compacted_ ? own_nnz_[0] : nnz_;  // stored nonzeros of K on this rank
+  out[3] = compacted_ ? own_nnz_[1] : nnz_;  // ... and of K^T
 }
 
 }  // namespace pdlp

@@ -332,6 +332,9 @@ class Solver {
   std::vector<int64_t> k_cuts_, kt_cuts_;  // world + 1 row boundaries of K and K^T
   DevBuf<unsigned> xmask_, ymask_;          // gather masks of x' / y' (sharded)
   int64_t push_values_ = 0, push_values_full_ = 0;  // values pushed per trial: masked / every peer
+  bool compacted_ = false;                          // sharded rank holding only its own operator rows
+  int64_t own_nnz_[2] = {0, 0};
+  void compact_own_rows();
   uint64_t plan_hash_ = 0;
   DevBuf<ShardSync> sync_;
   DevBuf<ShardView> shv_dev_;

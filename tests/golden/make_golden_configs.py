@@ -16,6 +16,13 @@ configs.json:
     solver.hpp:935-940): status, iterations, restarts, objectives.
 
     python tests/golden/make_golden_configs.py --reorder-drift [C2 C3 C4]
+    python tests/golden/make_golden_configs.py --solve C3 C4
+
+--solve adds the reference's own full solve at eps 1e-4 (solve(),
+solver.hpp:935-940; hours on one core for C4) to each entry: status,
+iterations, restarts, objectives.
+
+    python tests/golden/make_golden_configs.py --reorder-drift [C2 C3 C4]
 
 adds `reorder_drift` to each entry: how far the reference's own first N
 iterates move when only the summation order of the step-size sums (dx^2, dy^2,
@@ -137,6 +144,22 @@ def main() -> None:
             assert lp_hash(lp) == meta[name]["instance_sha256"]
             meta[name]["reorder_drift"] = reorder_drift(name, lp)
             print(f"{name}: {meta[name]['reorder_drift']} ({time.time() - t:.0f} s)", flush=True)
+            meta_path.write_text(json.dumps(meta, indent=1, sort_keys=True) + "\n")
+            del lp
+        return
+    if args and args[0] == "--solve":
+        meta_path = OUT / "configs.json"
+        for name in args[1:]:
+            lp = generators.config(name)
+            meta = json.loads(meta_path.read_text())
+            assert lp_hash(lp) == meta[name]["instance_sha256"]
+            t = time.time()
+            r = O.solve(lp, SolverParams(eps_optimal=1e-4, time_limit_seconds=1e9), "ref")
+            meta = json.loads(meta_path.read_text())  # re-read: other runs may have written meanwhile
+            meta[name]["solve_0.0001"] = {"status": str(r.status), "iterations": r.iterations,
+                                          "restarts": r.restarts, "primal_objective": r.info["primal_objective"],
+                                          "dual_objective": r.info["dual_objective"], "seconds": time.time() - t}
+            print(f"{name}: {meta[name]['solve_0.0001']}", flush=True)
             meta_path.write_text(json.dumps(meta, indent=1, sort_keys=True) + "\n")
             del lp
         return

@@ -22,6 +22,8 @@ the product's default) against the reference solver.
 * C4 (configs[3], 200M nonzeros): the first 20 iterates against the
   committed goldens (sampled entries and full-vector norms), parity mode
   bitwise and fast mode within the bar.
+* C3 and C4 solved to 1e-4 against the reference's own full solves
+  (status, objective within the tolerance).
 * C3, C4, C5 solved to 1e-4: the reference's termination check at the
   GPU's returned point (acceptance criterion 2 style, acceptance_main.cpp:
   79-154).
@@ -168,6 +170,24 @@ def test_c4_first_20_iterates_against_goldens(mode):
             worst = max(worst, *errs)
     print(f"C4 {mode}: worst relative error over 20 iterates (sampled max-norm, norms, eta, omega): {worst:.3e}")
     assert worst <= (1e-14 if mode == Mode.PARITY else fast_bar("C4")[1]), worst
+
+
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_full_solve_matches_reference(name):
+    """C3 and C4 solved to 1e-4 against the reference's own full solve
+    (configs.json `solve_0.0001`, make_golden_configs.py --solve: minutes on
+    one core for C3, hours for C4): same status, objectives within the solve
+    tolerance."""
+    want = meta()[name].get("solve_0.0001")
+    if want is None:
+        pytest.skip(f"no reference solve recorded for {name}")
+    lp = generators.config(name)
+    assert lp_hash(lp) == meta()[name]["instance_sha256"]
+    r = solve(lp, SolverParams(eps_optimal=1e-4, time_limit_seconds=600.0))
+    assert str(r.status) == want["status"] == "optimal"
+    obj, robj = r.info["primal_objective"], want["primal_objective"]
+    print(f"{name}: {r.iterations} iterations (reference {want['iterations']}), obj {obj!r} vs {robj!r}")
+    assert abs(obj - robj) <= 2.0 * 1e-4 * (1.0 + abs(robj)), (obj, robj)
 
 
 # ---------------------------------------------------------------------------

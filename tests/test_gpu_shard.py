@@ -140,6 +140,9 @@ def test_coupling_only_exchange_bitwise_and_volume(name, world, monkeypatch):
         full = g.solve()
     assert all(same(a, b) for a, b in zip(masked, full)), name
     pushed, a2a = sum(v["pushed"] for v in vol), sum(v["all_to_all"] for v in vol)
+    # per-rank operator storage: the ranks' rows of K and of K^T partition the nonzeros
+    assert sum(v["k_nnz"] for v in vol) == lp.nnz and sum(v["kt_nnz"] for v in vol) == lp.nnz
+    assert all(v["k_nnz"] < lp.nnz and v["kt_nnz"] < lp.nnz for v in vol)
     assert all(v["pushed"] == v["all_to_all"] for v in full_vol)
     assert pushed <= a2a
     print(f"{name} x{world}: {pushed} of {a2a} values pushed per trial ({pushed / a2a:.4f})")
