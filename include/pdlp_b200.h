@@ -387,6 +387,14 @@ int pdlp_shard_exchange(pdlp_handle* h, int64_t* out);
 /* Host-only: the row cuts (world + 1 each) of K = (G; A) and of K^T that a
  * world-way sharded solve of `lp` uses. No device work. */
 int pdlp_plan_shards(const pdlp_lp* lp, int32_t world, int64_t* k_cuts, int64_t* kt_cuts);
+/* Host-only: the gather masks of that partition (bit q of xmask[j]: a row of
+ * K owned by rank q holds column j; bit q of ymask[i]: row i holds a column
+ * owned by rank q; both optional, n and m entries) and, per rank, the x' / y'
+ * values a trial pushes to peers with the masks (pushed[world]) and with an
+ * all-to-all push (all_to_all[world]). No device work; the device builds the
+ * same masks at pdlp_create (pdlp_shard_exchange). */
+int pdlp_plan_exchange(const pdlp_lp* lp, int32_t world, int64_t* pushed, int64_t* all_to_all, uint32_t* xmask,
+                       uint32_t* ymask);
 
 /* ---- LP files (host I/O; no device work) ----------------------------- */
 

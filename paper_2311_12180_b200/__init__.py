@@ -15,8 +15,8 @@ from .lp import (
     SolverParams,
     SolveStatus,
 )
-from .api import (PdlpError, ShardGroup, ShardRank, Solver, device_count, load_library, parse_mps, plan_shards,
-                  read_mps, solve, solve_distributed, write_solution)
+from .api import (PdlpError, ShardGroup, ShardRank, Solver, device_count, load_library, parse_mps, plan_exchange,
+                  plan_shards, read_mps, solve, solve_distributed, write_solution)
 
 __all__ = [
     "CsrMatrix",
@@ -41,5 +41,6 @@ __all__ = [
     "ShardRank",
     "device_count",
     "plan_shards",
+    "plan_exchange",
     "solve_distributed",
 ]

@@ -81,6 +81,7 @@ def load_library(build_if_missing: bool = True) -> C.CDLL:
         "pdlp_shard_exchange": (C.c_int, [H, i64p]),
         "pdlp_pdhg_raw_step": (C.c_int, [H, dp, dp, C.c_double, C.c_double, dp, dp]),
         "pdlp_plan_shards": (C.c_int, [C.POINTER(abi.PdlpLp), C.c_int32, i64p, i64p]),
+        "pdlp_plan_exchange": (C.c_int, [C.POINTER(abi.PdlpLp), C.c_int32, i64p, i64p, C.c_void_p, C.c_void_p]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -280,6 +281,20 @@ def plan_shards(lp: GeneralFormLp, world: int) -> tuple[np.ndarray, np.ndarray]:
     return kc, ktc
 
 
+def plan_exchange(lp: GeneralFormLp, world: int) -> dict:
+    """Gather masks and per-rank exchange volumes of a world-way sharded solve
+    (pdlp_plan_exchange; host only, no GPU): xmask (n) / ymask (m) as uint32
+    bit sets of the ranks that gather each x' / y' value, and per rank the
+    values pushed per trial with the masks and with an all-to-all push."""
+    lib = load_library()
+    lpa = lp.to_abi()
+    pushed, a2a = np.zeros(world, np.int64), np.zeros(world, np.int64)
+    xm, ym = np.zeros(lp.num_variables, np.uint32), np.zeros(lp.num_constraints, np.uint32)
+    _check(lib.pdlp_plan_exchange(C.byref(lpa), world, abi.i64ptr(pushed), abi.i64ptr(a2a),
+                                  xm.ctypes.data_as(C.c_void_p), ym.ctypes.data_as(C.c_void_p)))
+    return {"pushed": pushed, "all_to_all": a2a, "xmask": xm, "ymask": ym}
+
+
 class ShardGroup:
     """All ranks of one row-sharded solve inside this process (the loopback
     transport: every rank gets its own stream and buffers, usually on one
@@ -460,7 +475,7 @@ def solve(lp: GeneralFormLp, params: SolverParams | None = None) -> SolveResult:
         return s.solve()
 
 
-__all__ = ["Solver", "ShardRank", "solve", "load_library", "default_params", "PdlpError", "library_path", "read_mps",
+__all__ = ["Solver", "ShardRank", "plan_exchange", "solve", "load_library", "default_params", "PdlpError", "library_path", "read_mps",
            "parse_mps", "write_solution", "MPS_FIXED", "MPS_FREE", "MPS_AUTO", "ShardGroup", "plan_shards",
            "csr_from_triplets",
            "solve_distributed"]

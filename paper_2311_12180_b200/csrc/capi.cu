@@ -266,6 +266,50 @@ int pdlp_shard_exchange(pdlp_handle* h, int64_t* out) {
   return guarded([&] { h->solver->shard_exchange(out); });
 }
 
+// Host-only twin of the device gather masks (kernels.cu shard_mask_kernel):
+// bit q of xmask[c] = a row of K owned by rank q holds column c; bit q of
+// ymask[r] = row r holds a column owned by rank q. Per rank, the x' / y'
+// values it pushes per trial with the masks and with an all-to-all push.
+int pdlp_plan_exchange(const pdlp_lp* lp, int32_t world, int64_t* pushed, int64_t* all_to_all, uint32_t* xmask,
+                       uint32_t* ymask) {
+  if (!lp || !pushed || !all_to_all) {
+    g_last_error = "null argument";
+    return PDLP_EINVAL;
+  }
+  return guarded([&] {
+    std::vector<int64_t> kc(size_t(world) + 1), ktc(size_t(world) + 1);
+    if (int rc = pdlp_plan_shards(lp, world, kc.data(), ktc.data()); rc != PDLP_OK)
+      throw std::invalid_argument(g_last_error);
+    const pdlp_csr& G = lp->inequality_matrix;
+    const pdlp_csr& A = lp->equality_matrix;
+    const int64_t m1 = G.num_rows, m2 = A.num_rows, n = lp->num_variables, m = m1 + m2;
+    std::vector<uint32_t> xm(size_t(n), 0u), ym(size_t(m), 0u);
+    auto owner = [](const std::vector<int64_t>& cuts, int64_t i) {
+      return int(std::upper_bound(cuts.begin() + 1, cuts.end(), i) - cuts.begin() - 1);
+    };
+    int64_t r = 0;
+    for (const pdlp_csr* c : {&G, &A})
+      for (int64_t i = 0; i < c->num_rows; ++i, ++r) {
+        const int pr = owner(kc, r);
+        for (int64_t k = c->row_offsets[i]; k < c->row_offsets[i + 1]; ++k) {
+          const int64_t j = c->col_indices ? c->col_indices[k] : c->col_indices32[k];
+          xm[size_t(j)] |= 1u << pr;
+          ym[size_t(r)] |= 1u << owner(ktc, j);
+        }
+      }
+    for (int q = 0; q < world; ++q) {
+      const uint32_t others = ((world >= 32 ? 0xffffffffu : ((1u << world) - 1u)) & ~(1u << q));
+      int64_t a = 0;
+      for (int64_t j = ktc[size_t(q)]; j < ktc[size_t(q) + 1]; ++j) a += __builtin_popcount(xm[size_t(j)] & others);
+      for (int64_t i = kc[size_t(q)]; i < kc[size_t(q) + 1]; ++i) a += __builtin_popcount(ym[size_t(i)] & others);
+      pushed[q] = a;
+      all_to_all[q] = ((ktc[size_t(q) + 1] - ktc[size_t(q)]) + (kc[size_t(q) + 1] - kc[size_t(q)])) * (world - 1);
+    }
+    if (xmask) std::copy(xm.begin(), xm.end(), xmask);
+    if (ymask) std::copy(ym.begin(), ym.end(), ymask);
+  });
+}
+
 int pdlp_plan_shards(const pdlp_lp* lp, int32_t world, int64_t* k_cuts, int64_t* kt_cuts) {
   if (!lp || !k_cuts || !kt_cuts) {
     g_last_error = "null argument";

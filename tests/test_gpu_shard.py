@@ -21,7 +21,7 @@ from pathlib import Path
 import numpy as np
 import pytest
 
-from paper_2311_12180_b200 import ShardGroup, Solver, SolverParams, SolveStatus, generators, solve
+from paper_2311_12180_b200 import ShardGroup, Solver, SolverParams, SolveStatus, generators, plan_exchange, solve
 from tests.test_gpu_parity import skewed_lp
 
 pytestmark = pytest.mark.gpu
@@ -140,6 +140,10 @@ def test_coupling_only_exchange_bitwise_and_volume(name, world, monkeypatch):
         full = g.solve()
     assert all(same(a, b) for a, b in zip(masked, full)), name
     pushed, a2a = sum(v["pushed"] for v in vol), sum(v["all_to_all"] for v in vol)
+    # the device's masks count what the host planner (pdlp_plan_exchange) plans
+    plan = plan_exchange(lp, world)
+    assert [v["pushed"] for v in vol] == plan["pushed"].tolist()
+    assert [v["all_to_all"] for v in vol] == plan["all_to_all"].tolist()
     # per-rank operator storage: the ranks' rows of K and of K^T partition the nonzeros
     assert sum(v["k_nnz"] for v in vol) == lp.nnz and sum(v["kt_nnz"] for v in vol) == lp.nnz
     assert all(v["k_nnz"] < lp.nnz and v["kt_nnz"] < lp.nnz for v in vol)
