@@ -135,8 +135,6 @@ Solver::Solver(const pdlp_lp& lp, const pdlp_params& params) : params_(params) {
     uint64_t keep = ~uint64_t(0);
     PDLP_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
   }
-  if (const char* e = std::getenv("PDLP_L2_FETCH"))  // L2 fetch granularity hint (A/B)
-    PDLP_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, size_t(std::atoi(e))));
   PDLP_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   if (!std::getenv("PDLP_NO_EVAL_FORK")) {
     PDLP_CUDA(cudaStreamCreateWithFlags(&fork_.s2, cudaStreamNonBlocking));
