@@ -13,6 +13,9 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <functional>
+#include <future>
+#include <memory>
 #include <mutex>
 #include <map>
 #include <cmath>
@@ -186,17 +189,16 @@ void Solver::setup(const pdlp_lp& lp) {
   nnz_ = G.nnz + A.nnz;
 
   objective_constant_ = lp.objective_constant;
-  c_.assign(lp.objective, lp.objective + n_);
-  l_.assign(lp.lower, lp.lower + n_);
-  u_.assign(lp.upper, lp.upper + n_);
-  q_.resize(m_);
-  std::copy(lp.inequality_rhs, lp.inequality_rhs + m1_, q_.begin());
-  std::copy(lp.equality_rhs, lp.equality_rhs + m2_, q_.begin() + m1_);
+  hc_ = lp.objective;
+  hl_ = lp.lower;
+  hu_ = lp.upper;
+  hh_ = lp.inequality_rhs;
+  hb_ = lp.equality_rhs;
   {  // termination_norms on the ORIGINAL instance (solver.hpp:157-163)
     double sh = 0.0, sb = 0.0, sc = 0.0;
-    for (int64_t i = 0; i < m1_; ++i) sh += q_[i] * q_[i];
-    for (int64_t i = m1_; i < m_; ++i) sb += q_[i] * q_[i];
-    for (double v : c_) sc += v * v;
+    for (int64_t i = 0; i < m1_; ++i) sh += hh_[i] * hh_[i];
+    for (int64_t i = 0; i < m2_; ++i) sb += hb_[i] * hb_[i];
+    for (int64_t j = 0; j < n_; ++j) sc += hc_[j] * hc_[j];
     rhs_norm_ = std::sqrt(sh + sb);
     obj_norm_ = std::sqrt(sc);
   }
@@ -218,6 +220,7 @@ void Solver::setup(const pdlp_lp& lp) {
   PDLP_CUDA(cudaMemcpyAsync(aoff.get(), A.row_offsets ? A.row_offsets : zero_off.data(),
                             (m2_ + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
   launch_build_rowptr(goff.get(), aoff.get(), m1_, m2_, G.nnz, k_rp_.get(), s);
+  mark("upload/rowptr");
   DevBuf<int> err(1);
   err.zero(s);
   int64_t off = 0;
@@ -233,11 +236,13 @@ void Solver::setup(const pdlp_lp& lp) {
         launch_narrow_cols(tmp.get(), k_col_.get() + off, c->nnz, int(n_), err.get(), s);
         PDLP_CUDA(cudaStreamSynchronize(s));
       }
+      mark("upload/cols");
       PDLP_CUDA(cudaMemcpyAsync(k_val_orig_.get() + off, c->values, c->nnz * sizeof(double),
                                 cudaMemcpyHostToDevice, s));
     }
     off += c->nnz;
   }
+  mark("upload/values");
   launch_check_cols(k_col_.get(), nnz_, int(n_), err.get(), s);
   launch_check_rows(k_rp_.get(), k_col_.get(), int(m_), err.get(), s);
   int herr = 0;
@@ -252,25 +257,38 @@ void Solver::setup(const pdlp_lp& lp) {
   mark("transpose");
 
   // original vectors on the device (evaluation on the unscaled LP)
-  auto up = [&](DevBuf<double>& d, const std::vector<double>& h) {
-    d.alloc(h.size());
-    if (!h.empty())
-      PDLP_CUDA(cudaMemcpyAsync(d.get(), h.data(), h.size() * sizeof(double),
-                                cudaMemcpyHostToDevice, s));
+  auto up = [&](DevBuf<double>& d, int64_t len, std::initializer_list<std::pair<const double*, int64_t>> parts) {
+    d.alloc(size_t(len));
+    int64_t at = 0;
+    for (const auto& pr : parts) {
+      if (pr.second > 0)
+        PDLP_CUDA(cudaMemcpyAsync(d.get() + at, pr.first, size_t(pr.second) * sizeof(double),
+                                  cudaMemcpyHostToDevice, s));
+      at += pr.second;
+    }
   };
-  up(c_orig_, c_);
-  up(l_orig_, l_);
-  up(u_orig_, u_);
-  up(q_orig_, q_);
+  up(c_orig_, n_, {{hc_, n_}});
+  up(l_orig_, n_, {{hl_, n_}});
+  up(u_orig_, n_, {{hu_, n_}});
+  up(q_orig_, m_, {{hh_, m1_}, {hb_, m2_}});
 
   precondition();
   mark("precondition");
 
   // tile plans (host planner over the offsets)
-  std::vector<int> rp_h(m_ + 1), rpt_h(n_ + 1);
-  PDLP_CUDA(cudaMemcpyAsync(rp_h.data(), k_rp_.get(), (m_ + 1) * sizeof(int),
+  // (page-locked, from the pool: no zero fill, full-speed D2H)
+  size_t rp_cap = 0, rpt_cap = 0;
+  std::unique_ptr<int, std::function<void(int*)>> rp_hold(
+      static_cast<int*>(pinned_pool_get(size_t(m_ + 1) * sizeof(int), &rp_cap)),
+      [&rp_cap](int* q) { pinned_pool_put(q, rp_cap); });
+  std::unique_ptr<int, std::function<void(int*)>> rpt_hold(
+      static_cast<int*>(pinned_pool_get(size_t(n_ + 1) * sizeof(int), &rpt_cap)),
+      [&rpt_cap](int* q) { pinned_pool_put(q, rpt_cap); });
+  int* rp_h = rp_hold.get();
+  int* rpt_h = rpt_hold.get();
+  PDLP_CUDA(cudaMemcpyAsync(rp_h, k_rp_.get(), (m_ + 1) * sizeof(int),
                             cudaMemcpyDeviceToHost, s));
-  PDLP_CUDA(cudaMemcpyAsync(rpt_h.data(), kt_rp_.get(), (n_ + 1) * sizeof(int),
+  PDLP_CUDA(cudaMemcpyAsync(rpt_h, kt_rp_.get(), (n_ + 1) * sizeof(int),
                             cudaMemcpyDeviceToHost, s));
   PDLP_CUDA(cudaStreamSynchronize(s));
   K_ = DevCsr{k_rp_.get(), k_col_.get(), k_val_.get(), k_val_orig_.get(), int(m_), int(n_), nnz_};
@@ -285,8 +303,8 @@ void Solver::setup(const pdlp_lp& lp) {
   k_cuts_ = {0, m_};
   kt_cuts_ = {0, n_};
   if (plan_world > 1) {
-    const std::vector<int64_t> kc = shard_cuts<int>(m_, rp_h.data(), plan_world);
-    const std::vector<int64_t> ktc = shard_cuts<int>(n_, rpt_h.data(), plan_world);
+    const std::vector<int64_t> kc = shard_cuts<int>(m_, rp_h, plan_world);
+    const std::vector<int64_t> ktc = shard_cuts<int>(n_, rpt_h, plan_world);
     kbrk.assign(kc.begin() + 1, kc.end() - 1);
     ktbrk.assign(ktc.begin() + 1, ktc.end() - 1);
     if (world_ > 1) {
@@ -318,10 +336,10 @@ void Solver::setup(const pdlp_lp& lp) {
     kc_p = &kcon;
     ktc_p = &ktcon;
   }
-  build_plan(k_it_, K_, rp_h, kIterGeom, kbrk, r0, r1, kc_p);
-  build_plan(kt_it_, KT_, rpt_h, kIterGeom, ktbrk, c0, c1, ktc_p);
-  build_plan(k_ev_, K_, rp_h, kEvalGeom, kbrk, r0, r1, kc_p);
-  build_plan(kt_ev_, KT_, rpt_h, kEvalGeom, ktbrk, c0, c1, ktc_p);
+  build_plan(k_it_, K_, rp_h, m_, kIterGeom, kbrk, r0, r1, kc_p);
+  build_plan(kt_it_, KT_, rpt_h, n_, kIterGeom, ktbrk, c0, c1, ktc_p);
+  build_plan(k_ev_, K_, rp_h, m_, kEvalGeom, kbrk, r0, r1, kc_p);
+  build_plan(kt_ev_, KT_, rpt_h, n_, kEvalGeom, ktbrk, c0, c1, ktc_p);
   if (trace) {
     for (const auto& pr : {std::make_pair("K", &k_it_), std::make_pair("KT", &kt_it_)}) {
       const TilePlan& tp = pr.second->plan;
@@ -367,6 +385,8 @@ void Solver::setup(const pdlp_lp& lp) {
   set_kernel_attributes();
   pin_iterates_in_l2();
   mark("attributes");
+  if (omega_job_.valid()) omega_job_.get();
+  hc_ = hl_ = hu_ = hh_ = hb_ = nullptr;  // the caller's arrays are not ours past pdlp_create
 }
 
 // Decides whether `op` (rows x cols) gets column panels and builds them: the
@@ -478,7 +498,7 @@ void Solver::primal_step(int mode_override, unsigned long long cond, int use_con
     launch_primal(KT_, it_, parity(), mode_override, stream_, cond, use_cond);
 }
 
-void Solver::build_plan(OpPlan& p, const DevCsr& base, const std::vector<int>& rp,
+void Solver::build_plan(OpPlan& p, const DevCsr& base, const int* rp, int64_t rows,
                         const TileGeom& g, const std::vector<int64_t>& breaks, int64_t r0,
                         int64_t r1, const std::vector<uint8_t>* contig) {
   // planner thresholds: env overrides are a tuning aid (clamped to the geometry)
@@ -498,12 +518,12 @@ void Solver::build_plan(OpPlan& p, const DevCsr& base, const std::vector<int>& r
   // 1e-10 bar (their full-size configs use 4096 anyway).
   int snnz_def = g.stream_nnz;
   if (&g == &kIterGeom) {
-    const int64_t nnz = rp.empty() ? 0 : int64_t(rp.back());
+    const int64_t nnz = int64_t(rp[rows]);
     if (nnz >= (int64_t(1) << 16) && nnz < (int64_t(1) << 18)) snnz_def = 1024;
   }
   const int snnz = std::max(64, std::min(knob("PDLP_STREAM_NNZ", snnz_def), g.stream_nnz));
   const int srows = std::max(kThreads, std::min(knob("PDLP_STREAM_ROWS", g.stream_rows), g.stream_rows));
-  p.plan = plan_tiles<int>(int64_t(rp.size()) - 1, rp.data(), parity(), std::min(smax, snnz), wmax, cnnz,
+  p.plan = plan_tiles<int>(rows, rp, parity(), std::min(smax, snnz), wmax, cnnz,
                            snnz, srows, kThreads, lane, breaks, contig);
   const std::vector<Tile>& th = p.plan.tiles;
   p.tiles.alloc(th.size());
@@ -514,7 +534,7 @@ void Solver::build_plan(OpPlan& p, const DevCsr& base, const std::vector<int>& r
   p.ctr.zero(stream_);
   p.csr = base;
   p.csr.tiles = p.tiles.get();
-  const auto own = tile_range(p.plan, r0, r1, int64_t(rp.size()) - 1);  // this rank's tiles (all of them unsharded)
+  const auto own = tile_range(p.plan, r0, r1, rows);  // this rank's tiles (all of them unsharded)
   p.csr.tile0 = own.first;
   p.csr.ntiles = own.second - own.first;
   p.csr.chunk_slots = p.plan.chunk_slots;
@@ -622,18 +642,22 @@ void Solver::precondition() {
   // the scaled vectors are the same products the device formed.
   // norm2 of the scaled c and q, summed in index order as norm2 of the
   // materialised vectors would be (no n-vector temporaries on the host)
-  double sc = 0.0, sq = 0.0;
-  for (int64_t j = 0; j < n_; ++j) {
-    const double v = c_[j] * d2_[j];
-    sc += v * v;
-  }
-  for (int64_t i = 0; i < m_; ++i) {
-    const double v = q_[i] * d1_[i];
-    sq += v * v;
-  }
-  const double cn2 = std::sqrt(sc), qn2 = std::sqrt(sq);
-  const double w = (cn2 > params_.eps_zero && qn2 > params_.eps_zero) ? cn2 / qn2 : 1.0;
-  omega0_ = sclamp(w, params_.omega_min, params_.omega_max);
+  // (two sequential sums of tens of millions of terms: on a host thread while
+  // the rest of setup runs; joined at its end)
+  omega_job_ = std::async(std::launch::async, [this] {
+    double sc = 0.0, sq = 0.0;
+    for (int64_t j = 0; j < n_; ++j) {
+      const double v = hc_[j] * d2_[j];
+      sc += v * v;
+    }
+    for (int64_t i = 0; i < m_; ++i) {
+      const double v = hq(i) * d1_[i];
+      sq += v * v;
+    }
+    const double cn2 = std::sqrt(sc), qn2 = std::sqrt(sq);
+    const double w = (cn2 > params_.eps_zero && qn2 > params_.eps_zero) ? cn2 / qn2 : 1.0;
+    omega0_ = sclamp(w, params_.omega_min, params_.omega_max);
+  });
 }
 
 // The iterate buffers the SpMVs gather from (x for K x', y for K'y') stay in
@@ -750,7 +774,7 @@ void Solver::allocate_iteration() {
     // min(max(v, l), u) == max(v, 0) bitwise, and the bound streams are skipped
     bool nonneg = true;
     for (int64_t j = 0; j < n_ && nonneg; ++j)
-      nonneg = l_[j] == 0.0 && !std::signbit(l_[j]) && u_[j] == INFINITY;
+      nonneg = hl_[j] == 0.0 && !std::signbit(hl_[j]) && hu_[j] == INFINITY;
     it.nonneg = nonneg ? 1 : 0;
   }
   it.avg_blocks = avg_blocks;

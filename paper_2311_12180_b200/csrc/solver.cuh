@@ -9,6 +9,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <future>
 #include <vector>
 
 #include "../../include/pdlp_b200.h"
@@ -214,7 +215,8 @@ class Solver {
     DevBuf<unsigned> ctr;
     DevCsr csr{};
   };
-  void build_plan(OpPlan& p, const DevCsr& base, const std::vector<int>& rp, const TileGeom& g,
+  // rp: host copy of the operator's rows + 1 row offsets
+  void build_plan(OpPlan& p, const DevCsr& base, const int* rp, int64_t rows, const TileGeom& g,
                   const std::vector<int64_t>& breaks, int64_t r0, int64_t r1,
                   const std::vector<uint8_t>* contig = nullptr);
   void shard_view_upload();
@@ -261,7 +263,10 @@ class Solver {
   double objective_constant_ = 0.0;
 
   // host copies of the original vectors (evaluation bookkeeping is host-side)
-  std::vector<double> c_, q_, l_, u_;
+  // the caller's objective, bounds and right-hand sides: read during
+  // pdlp_create only (setup), never kept
+  const double *hc_ = nullptr, *hl_ = nullptr, *hu_ = nullptr, *hh_ = nullptr, *hb_ = nullptr;
+  double hq(int64_t i) const { return i < m1_ ? hh_[i] : hb_[i - m1_]; }
   PinnedVec d1_, d2_;  // the scaling, downloaded once at setup
   double rhs_norm_ = 0.0, obj_norm_ = 0.0;  // termination_norms (solver.hpp:157-163)
   double eta_hat0_ = 1.0, omega0_ = 1.0;
@@ -343,6 +348,9 @@ class Solver {
   std::shared_ptr<LocalGroup> group_;
   PhaseFn phase_;
   std::vector<void*> ipc_opened_;
+  // initialize_primal_weight's host sums (setup); declared last so that it
+  // is destroyed (joined) before the members it reads
+  std::future<void> omega_job_;
 };
 
 }  // namespace pdlp
