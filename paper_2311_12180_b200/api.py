@@ -115,7 +115,7 @@ class Solver:
     def __init__(self, lp: GeneralFormLp, params: SolverParams | None = None):
         self._lib = load_library()
         self.params = params or SolverParams()
-        lp.validate()  # the C ABI reads the arrays through raw pointers
+        lp.validate_shapes()  # the C ABI reads the arrays through raw pointers (it checks the values itself)
         self._lp = lp  # keeps the host arrays alive during create
         self._h = C.c_void_p()
         lpa = lp.to_abi()

@@ -177,6 +177,21 @@ class GeneralFormLp:
     def validate(self) -> None:
         """GeneralFormLp::validate (lp_model.hpp:45-72), plus the CSR storage
         checks the raw-pointer C ABI needs."""
+        self.validate_shapes()
+        nan = np.nonzero(np.isnan(self.lower) | np.isnan(self.upper))[0]
+        if nan.size:
+            raise ValueError(f"lp: NaN bound on variable {int(nan[0])}")
+        bad = np.nonzero((self.lower > self.upper) | (self.lower == np.inf) | (self.upper == -np.inf))[0]
+        if bad.size:
+            raise ValueError(f"lp: empty bound interval on variable {int(bad[0])}")
+        if np.isnan(self.objective).any():
+            raise ValueError("lp: NaN objective entry")
+
+    def validate_shapes(self) -> None:
+        """The array-length half of validate(): what the raw-pointer C ABI
+        cannot check itself (it would read past a short array). The value
+        checks (NaN and empty bounds, NaN objective) are repeated by
+        pdlp_create with the same messages."""
         for name, M in (("inequality", self.inequality_matrix), ("equality", self.equality_matrix)):
             if M.row_offsets.size != M.num_rows + 1:
                 raise ValueError(f"lp: {name} matrix row_offsets must have num_rows + 1 entries")
@@ -191,14 +206,6 @@ class GeneralFormLp:
             raise ValueError("lp: rhs length does not match row count")
         if self.lower.size != n or self.upper.size != n:
             raise ValueError("lp: bound vectors must have length n")
-        nan = np.nonzero(np.isnan(self.lower) | np.isnan(self.upper))[0]
-        if nan.size:
-            raise ValueError(f"lp: NaN bound on variable {int(nan[0])}")
-        bad = np.nonzero((self.lower > self.upper) | (self.lower == np.inf) | (self.upper == -np.inf))[0]
-        if bad.size:
-            raise ValueError(f"lp: empty bound interval on variable {int(bad[0])}")
-        if np.isnan(self.objective).any():
-            raise ValueError("lp: NaN objective entry")
 
     def to_abi(self) -> abi.PdlpLp:
         s = abi.PdlpLp()
