@@ -185,7 +185,10 @@ __device__ __forceinline__ void dual_tail_decision(const DevIter& it, DevState* 
 // the decision will start from. Parity mode keeps the decision here (last CTA),
 // where the reference-order sequential sums run.
 template <bool kSeq, bool kShard>
-__global__ void __launch_bounds__(kThreads, 4) dual_kernel(DevCsr K, DevIter it,
+#ifndef PDLP_ITER_CTAS
+#define PDLP_ITER_CTAS 4
+#endif
+__global__ void __launch_bounds__(kThreads, PDLP_ITER_CTAS) dual_kernel(DevCsr K, DevIter it,
                                                            cudaGraphConditionalHandle cond,
                                                            int use_cond) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -359,7 +362,7 @@ __global__ void chain_decide_kernel(DevState* st, const EvalOut* e, ChainConsts 
 // solve: retry; after a restart: restart). Otherwise the fast mode takes the
 // step decision first (all CTAs, CTA 0 commits it), parity mode reads it.
 template <bool kSeq, bool kNonneg, bool kShard>
-__global__ void __launch_bounds__(kThreads, 4) primal_kernel(DevCsr KT, DevIter it, int mode_override,
+__global__ void __launch_bounds__(kThreads, PDLP_ITER_CTAS) primal_kernel(DevCsr KT, DevIter it, int mode_override,
                                                              cudaGraphConditionalHandle cond,
                                                              int use_cond) {
   extern __shared__ __align__(16) unsigned char smem[];

@@ -393,8 +393,10 @@ void Solver::setup(const pdlp_lp& lp) {
 // gathered vector must exceed one panel's L2 budget (PDLP_PANEL_MB, default
 // 48 MB) and the rows must scatter over it (on average across at least half of
 // min(panels, row length) panels, i.e. no locality a single pass could use);
-// no row may hold more than 255 entries in one panel. PDLP_PANELS=1 forces
-// panels of PDLP_PANEL_WIDTH columns (tests); =0 disables them.
+// no row may hold more than 255 entries in one panel. Operators past 64 M
+// nonzeros that fail the scatter test run as a single panel (below).
+// PDLP_PANELS=1 forces panels of PDLP_PANEL_WIDTH columns (tests); =0
+// disables them.
 void Solver::build_panels(PanelOp& po, const DevCsr& op, int rows, int cols, const char* which) {
   cudaStream_t s = stream_;
   const char* force = std::getenv("PDLP_PANELS");
@@ -412,9 +414,17 @@ void Solver::build_panels(PanelOp& po, const DevCsr& op, int rows, int cols, con
     width = std::max(1, std::atoi(std::getenv("PDLP_PANEL_WIDTH")));
     panels = int((int64_t(cols) + width - 1) / width);
   }
-  if (panels < 2 || rows < 1 || op.nnz < 1) return;
-  if (int64_t(panels) * rows >= int64_t(std::numeric_limits<int32_t>::max()) - 1024) return;
-  if (!forced) {
+  if (rows < 1 || op.nnz < 1) return;
+  // operators too large for L2 whose rows stay local (C5's staircase) still
+  // run as one panel: the sweep's count-byte rows and fused final pass beat
+  // the tiled kernels there (C5 58.8 -> 67.1 it/s; profiles/r02p1_ab_single_panel.jsonl)
+  const bool single_ok = !forced && op.nnz >= (int64_t(1) << 26) && !std::getenv("PDLP_NO_SINGLE_PANEL");
+  bool single = false;
+  if (panels < 2 && !forced) {
+    if (!single_ok) return;
+    single = true;
+  }
+  if (!single && !forced) {
     DevBuf<unsigned long long> d{static_cast<size_t>(1)};
     d.zero(s);
     launch_panel_spread(op.rp, op.col, rows, width, d.get(), s);
@@ -423,8 +433,16 @@ void Solver::build_panels(PanelOp& po, const DevCsr& op, int rows, int cols, con
     PDLP_CUDA(cudaStreamSynchronize(s));
     const double per_row = double(distinct) / double(rows);
     const double avg_len = double(op.nnz) / double(rows);
-    if (per_row < 0.5 * std::min(double(panels), avg_len)) return;
+    if (per_row < 0.5 * std::min(double(panels), avg_len)) {
+      if (!single_ok) return;
+      single = true;
+    }
   }
+  if (single) {
+    panels = 1;
+    width = cols;
+  }
+  if (int64_t(panels) * rows >= int64_t(std::numeric_limits<int32_t>::max()) - 1024) return;
   // panel-major order: entry k of row r, column c goes to stacked row
   // (c / width) * rows + r; a stable radix sort keeps each row's columns in
   // increasing order
