@@ -477,7 +477,7 @@ def test_gpu_from_triplets_large_matches_host_csr():
 # column panels (panels.cu): forced on small instances with narrow panels
 # ---------------------------------------------------------------------------
 
-@pytest.mark.parametrize("width", ["700", "4096"])
+@pytest.mark.parametrize("width", ["700", "4096", "1000000000"])  # the last: one panel (C5's single-panel sweep)
 def test_column_panel_spmv_bitwise_sequential(width, monkeypatch):
     """The panel sweep sums every row by one thread in column order, from 0.0:
     bitwise equal to the reference's sequential spmv (sparse_matrix.hpp:117-132)
