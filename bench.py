@@ -395,6 +395,17 @@ def run_ours(args):
         traffic = profile_traffic(CONFIG).get(dom, {})
     solver.close()
 
+    # the CPU baseline child ends before the end-to-end loop, whose host work
+    # (uploads, setup) it would otherwise slow down
+    cpu = None
+    if cpu_proc is not None:
+        out, err = cpu_proc.communicate(timeout=1800)
+        try:
+            cpu = json.loads(out.strip().splitlines()[-1])
+        except (ValueError, IndexError):
+            cpu = {"value": None, "unit": UNIT, "kind": "reference", "cores": 1,
+                   "sample": f"failed: {err.strip()[-300:]}"}
+
     # ---- e2e through the C-ABI with host buffers ----
     e2e_steps = max(1, min(args.steps, E2E_STEPS))
     e2e_iters, e2e_s = 0, 0.0
@@ -409,7 +420,7 @@ def run_ours(args):
         t1 = time.perf_counter()
         r2 = s2.solve()  # pdlp_solve + pdlp_get_solution (D2H)
         t2 = time.perf_counter()
-        s2.close()
+        s2.close()  # pdlp_destroy
         torch.cuda.synchronize()
         t3 = time.perf_counter()
         e2e_s += t3 - t0
@@ -423,14 +434,6 @@ def run_ours(args):
 
     c2 = c2_extra(device) if rank == 0 and world == 1 and not args.no_c2 else None
 
-    cpu = None
-    if cpu_proc is not None:
-        out, err = cpu_proc.communicate(timeout=1800)
-        try:
-            cpu = json.loads(out.strip().splitlines()[-1])
-        except (ValueError, IndexError):
-            cpu = {"value": None, "unit": UNIT, "kind": "reference", "cores": 1,
-                   "sample": f"failed: {err.strip()[-300:]}"}
 
     if rank == 0:
         if world == 1:
