@@ -114,6 +114,7 @@ struct PanelView {
   const int* boff;           // [panels][nblk + 1] first entry of each 1024-row block
   double* acc;               // [rows] running row sums between passes
   int rows, rows_pad, nblk, panels;
+  int transposed;            // 1: the operator is K^T (its sweeps stage larger rounds)
 };
 void launch_panel_keys(const int* row_of, const int* col, int64_t nnz, int width, int rows, int* keys,
                        cudaStream_t s);

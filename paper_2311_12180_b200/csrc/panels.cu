@@ -85,8 +85,14 @@ constexpr int kSweepRPT = kSweepRows / kThreads;
 // passes, 5 / 4 for the dual / primal final passes (C4: K 1.70 -> 1.44 ms,
 // whole iteration 234 -> 250 it/s; the passes are latency-bound, so resident
 // CTAs matter more than loads in flight per thread)
-#ifndef PDLP_SWEEP_CHUNK
-#define PDLP_SWEEP_CHUNK 1536
+#ifndef PDLP_SWEEP_CHUNK_K
+#define PDLP_SWEEP_CHUNK_K 1536
+#endif
+// K^T blocks hold ~1.7 k entries on C4 (5 per row over 3 panels): a 1792-entry
+// stage keeps them in one round (K^T 1.45 -> 1.31 ms), while K's ~1.46 k
+// entries per block run faster in 1536
+#ifndef PDLP_SWEEP_CHUNK_T
+#define PDLP_SWEEP_CHUNK_T 1792
 #endif
 #ifndef PDLP_SWEEP_CTAS
 #define PDLP_SWEEP_CTAS 6
@@ -104,16 +110,17 @@ constexpr int kSweepRPT = kSweepRows / kThreads;
 #define PDLP_SWEEP_STREAM_IO 1
 #endif
 constexpr bool kSweepStreamIO = PDLP_SWEEP_STREAM_IO != 0;
-constexpr int kSweepChunk = PDLP_SWEEP_CHUNK;      // products staged per round (12 KB)
-constexpr int kSweepPer = kSweepChunk / kThreads;  // entries per thread per round, all in flight
+constexpr int kChunkK = PDLP_SWEEP_CHUNK_K;  // products staged per round: sweeps over K
+constexpr int kChunkT = PDLP_SWEEP_CHUNK_T;  // ... over K^T
 constexpr int kSweepCtasPerSm = PDLP_SWEEP_CTAS;
 
 static_assert(kSweepRPT == 4 || kSweepRPT == 8, "four or eight count bytes and rows per thread");
 
+template <int CH>
 struct SweepSmem {
   int off[kSweepRows + 1];
   int warp[kWarps + 1];
-  double prod[kSweepChunk];
+  double prod[CH];
 };
 
 // ---- setup -----------------------------------------------------------------
@@ -226,8 +233,11 @@ __device__ __forceinline__ int block_excl_scan(int v, int* s_warp /* kWarps + 1 
 // Continues the running sums acc[i] of this thread's rows b R + tid + i kThreads
 // over panel p of v (acc[] = 0.0 at p = 0, else the sums loaded from `acc`);
 // returns a bit per row with entries in this panel.
+template <int CH>
 __device__ __forceinline__ unsigned sweep_block(const SweepOp& op, int p, int b, const double* __restrict__ v,
-                                                double (&acc)[kSweepRPT], SweepSmem& sm) {
+                                                double (&acc)[kSweepRPT], SweepSmem<CH>& sm) {
+  constexpr int kSweepChunk = CH;                    // entries staged per round
+  constexpr int kSweepPer = CH / kThreads;           // entries per thread per round, all in flight
   const int tid = threadIdx.x;
   const uint64_t ef = l2_evict_first_policy();
   // independent loads first: the block's entry range, its count bytes, the sums
@@ -310,7 +320,7 @@ __device__ __forceinline__ unsigned sweep_block(const SweepOp& op, int p, int b,
 template <bool kPrimal>
 __global__ void __launch_bounds__(kThreads, kSweepCtasPerSm) sweep_pass_kernel(SweepOp op, DevIter it, int p,
                                                                              int mode_override) {
-  __shared__ SweepSmem sm;
+  __shared__ SweepSmem<kPrimal ? kChunkT : kChunkK> sm;
   griddep_wait();
   const DevState* st = it.st;
   const double* src;
@@ -339,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, kSweepCtasPerSm) sweep_pass_kernel(S
 // b >= 1 finishes rows [(b-1) R, b R) and applies the dual update (DualEpi)
 // with its partials at slot b-1.
 __global__ void __launch_bounds__(kThreads, PDLP_SWEEP_CTAS_DUALF) sweep_dual_final_kernel(SweepOp op, DevIter it) {
-  __shared__ SweepSmem sm;
+  __shared__ SweepSmem<kChunkK> sm;
   griddep_wait();
   DevState* st = it.st;
   const bool parked = st->failure || st->window_accepts >= st->window_target;
@@ -387,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, PDLP_SWEEP_CTAS_DUALF) sweep_dual_fi
 template <bool kNonneg>
 __global__ void __launch_bounds__(kThreads, PDLP_SWEEP_CTAS_PRIMALF) sweep_primal_final_kernel(SweepOp op, DevIter it,
                                                                                      int mode_override) {
-  __shared__ SweepSmem sm;
+  __shared__ SweepSmem<kChunkT> sm;
   griddep_wait();
   DevState* st = it.st;
   const DevState& s = *st;
@@ -464,9 +474,10 @@ __global__ void __launch_bounds__(kThreads, PDLP_SWEEP_CTAS_PRIMALF) sweep_prima
 
 // Plain SpMV through the panel sweep (bench / kernel parity): out = A v, the
 // last pass storing the sums.
+template <int CH>
 __global__ void __launch_bounds__(kThreads, kSweepCtasPerSm) sweep_spmv_kernel(SweepOp op, const double* v, int p,
                                                                              double* out) {
-  __shared__ SweepSmem sm;
+  __shared__ SweepSmem<CH> sm;
   const int b = blockIdx.x;
   const int r0 = b * kSweepRows + threadIdx.x;
   double acc[kSweepRPT];
@@ -522,7 +533,10 @@ void launch_panel_primal(const PanelView& ktp, const DevIter& it, int mode_overr
 void launch_panel_spmv(const PanelView& pv, const double* v, double* out, cudaStream_t s) {
   const SweepOp& op = pv;
   for (int p = 0; p < op.panels; ++p) {
-    sweep_spmv_kernel<<<op.nblk, kThreads, 0, s>>>(op, v, p, out);
+    if (op.transposed)
+      sweep_spmv_kernel<kChunkT><<<op.nblk, kThreads, 0, s>>>(op, v, p, out);
+    else
+      sweep_spmv_kernel<kChunkK><<<op.nblk, kThreads, 0, s>>>(op, v, p, out);
     PDLP_CUDA(cudaGetLastError());
   }
 }

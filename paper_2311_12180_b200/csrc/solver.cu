@@ -496,7 +496,7 @@ void Solver::build_panels(PanelOp& po, const DevCsr& op, int rows, int cols, con
   po.panels = panels;
   po.width = width;
   po.view = PanelView{po.col.get(), po.val.get(), po.cnt.get(), po.boff.get(), po.acc.get(),
-                      rows, rows_pad, nblk, panels};
+                      rows, rows_pad, nblk, panels, kt ? 1 : 0};
   if (std::getenv("PDLP_TRACE_SETUP"))
     std::fprintf(stderr, "[pdlp setup] %s: %d column panels of %d columns, %d row blocks\n", which, panels,
                  width, nblk);
